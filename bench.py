@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark of the MPDATA transport step on B200 (contract: one JSON line on rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[2], the grid of the paper's Fig. 15): one
+fused MPDATA transport step on the periodic 279 x 256 x 80 patch
+(71,424 vertices = the paper's node count, 214,272 edges, 80 levels), fp64,
+inputs as the reference's ``_transport_setup`` (gaussian-bump density,
+U[-0.5,0.5) velocities, rho = 1, uniform geometry, dt = 0.1, pivbz = 1).
+
+* value: grid-point updates/s (V*K per step / device time), inputs resident in
+  HBM; each timed step is bracketed by CUDA events on the launching stream and
+  preceded (outside the events) by a 256 MiB L2 flush, so no step reads the
+  previous step's data from L2.
+* e2e: the same metric through the public flat-array API (StructuredStepper)
+  with pinned host buffers: per step H2D of pd/vn/wn/rho, on-GPU reorder into
+  the structured layout, fused step, reorder back, D2H of pd_out.
+* roofline: algorithmic bytes B_comp per step / average step time, against
+  the measured HBM copy bandwidth (MEASURED_PEAKS.json).
+* cpu_baseline / --impl reference: the reference algorithm restated in C
+  (oracle/c, bitwise equal to the reference, OpenMP over all host cores).
+* N > 1: weak scaling, one 279-row strip per rank of a (279*N) x 256 x 80
+  patch, row-strip decomposition with a per-step halo exchange (NCCL).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MPDATA grid-point updates/s & effective HBM GB/s (frac of peak) at 1/2/4/8 B200"
+UNIT = "grid-point updates/s"
+ROWS, COLS, LEVELS = 279, 256, 80
+DT, PIVBZ = 0.1, 1.0
+WORKLOAD = "MPDATA full step, 71424-node/214272-edge/80-level periodic patch (279x256x80), fp64"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy, burst)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (the reference algorithm restated in C; test/baseline infrastructure)
+
+
+def cpu_reference_steps(steps: int, warmup: int, budget_s: float | None = None):
+    from oracle import c_oracle
+    from oracle import tsg_oracle as O
+
+    inp = O.transport_inputs(ROWS, COLS, LEVELS, 0, "uniform", "gaussian-bump", "one")
+    e2v = O.neighbor_table(ROWS, COLS, "edges", "vertices")
+    v2e = O.neighbor_table(ROWS, COLS, "vertices", "edges")
+    args = (e2v, v2e, inp["signs"], inp["dual"], inp["pd"], inp["vn"], inp["wn"], inp["rho"], DT, PIVBZ)
+    out = None
+    for _ in range(warmup):
+        out = c_oracle.transport_step(*args, out=out)
+    times = []
+    t_begin = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        out = c_oracle.transport_step(*args, out=out)
+        times.append(time.perf_counter() - t0)
+        if budget_s is None and len(times) >= steps:
+            break
+        if budget_s is not None and (time.perf_counter() - t_begin > budget_s and len(times) >= 3):
+            break
+    return times, c_oracle.threads()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    times, threads = cpu_reference_steps(args.steps, args.warmup)
+    t = sum(times) / len(times)
+    value = ROWS * COLS * LEVELS / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "rows": ROWS, "cols": COLS, "levels": LEVELS},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"full {ROWS}x{COLS}x{LEVELS} step x {len(times)} "
+                                   "(reference.transport_step restated in C, oracle/c)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1908_06094_b200 import PatchSpec, StructuredStepper, _lib
+    from paper_1908_06094_b200.workloads import (mpdata_2d_bytes, mpdata_algorithmic_bytes,
+                                                 paper_model_bytes, transport_inputs)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    if args.variant:
+        _lib.check(_lib.lib().tsg_set_fused_variant(args.variant) < 0)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    V, K = ROWS * COLS, LEVELS
+    if world > 1:
+        from paper_1908_06094_b200.distributed import StripStepper
+
+        stepper = StripStepper(ROWS * world, COLS, K, rank, world, seed=0)
+    else:
+        inp = transport_inputs(ROWS, COLS, K, 0, "uniform", "gaussian-bump", "one")
+        stepper = StructuredStepper(PatchSpec(ROWS, COLS, K))
+        stepper.set_geometry(inp["signs"], inp["dual"])
+        stepper.upload(inp["pd"], inp["vn"], inp["wn"], inp["rho"])
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+
+    for _ in range(args.warmup):
+        stepper.step(DT, PIVBZ)
+        stepper.swap()
+    torch.cuda.synchronize()
+    barrier()
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        barrier()
+        torch.cuda.synchronize()
+        t_wall0 = time.perf_counter()
+        for s in range(args.steps):
+            flush.fill_(float(s))  # evict the previous step's data from L2 (outside the events)
+            evs[s][0].record(stream)
+            stepper.step(DT, PIVBZ)
+            evs[s][1].record(stream)
+            stepper.swap()
+        torch.cuda.synchronize()
+        barrier()
+        t_wall = time.perf_counter() - t_wall0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_s = sum(step_ms) / 1e3
+    if world > 1:
+        t = torch.tensor([total_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_s = float(t.item())
+    mean_step = total_s / args.steps
+    value = world * V * K / mean_step
+
+    # e2e through the public flat API from pinned host buffers (rank 0 / N=1 only)
+    e2e = None
+    if world == 1:
+        pinned = {n: torch.from_numpy(np.ascontiguousarray(inp[n])).pin_memory()
+                  for n in ("pd", "vn", "wn", "rho")}
+        out = torch.empty((V, K), dtype=torch.float64).pin_memory()
+        h2d = sum(t.numel() * 8 for t in pinned.values())
+        d2h = out.numel() * 8
+        e2e_steps = max(3, min(args.steps, 30))
+        for _ in range(2):
+            stepper.upload(pinned["pd"], pinned["vn"], pinned["wn"], pinned["rho"])
+            stepper.step(DT, PIVBZ)
+            stepper.download(out)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            stepper.upload(pinned["pd"], pinned["vn"], pinned["wn"], pinned["rho"])
+            stepper.step(DT, PIVBZ)
+            stepper.download(out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_e2e = e0.elapsed_time(e1) / 1e3 / e2e_steps
+        e2e = {"value": V * K / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3,
+               "api": "StructuredStepper.upload/step/download (flat canonical arrays, pinned)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = _peaks()
+    bcomp = mpdata_algorithmic_bytes(ROWS, COLS, K)
+    achieved = bcomp / mean_step / 1e9
+    traffic = None
+    tfile = ROOT / "profiles" / "fused_traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+    from paper_1908_06094_b200._lib import lib as _l
+    import ctypes
+
+    vi = [ctypes.c_int() for _ in range(6)]
+    _l().tsg_fused_variant_info(0, *[ctypes.byref(x) for x in vi])
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        times, threads = cpu_reference_steps(0, 1, budget_s=args.cpu_seconds)
+        tc = statistics.median(times)
+        cpu = {"value": V * K / tc, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"full {ROWS}x{COLS}x{K} step x {len(times)} (median), "
+                         "reference.transport_step restated in C (oracle/c), OpenMP"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": mean_step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "rows": ROWS * world, "cols": COLS, "levels": K,
+                   "rows_per_gpu": ROWS, "vertices": V * world, "edges": 3 * V * world,
+                   "dt": DT, "pivbz": PIVBZ, "parallelism": f"row-strips x{world}",
+                   "l2": "256 MiB L2 flush before every timed step (outside the events)",
+                   "fused_tile": {"ti": vi[0].value, "tj": vi[1].value, "kc": vi[2].value,
+                                  "stages": vi[3].value, "threads": vi[4].value,
+                                  "smem_bytes": vi[5].value}},
+        "effective_gbs": achieved,
+        "paper_model_gbs": paper_model_bytes(ROWS, COLS, K) / mean_step / 1e9,
+        "stage_updates_per_s": world * V * (6 * K + 1) / mean_step,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bcomp,
+                     "bytes_2d_per_launch": mpdata_2d_bytes(ROWS, COLS)},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+        "clocks": clocks.summary(),
+        "timed_wall_s": t_wall,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[1])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--variant", type=int, default=0, help="fused tile variant (0 = default)")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

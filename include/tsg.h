@@ -1,0 +1,183 @@
+/* tsg.h -- C ABI of the B200-native MPDATA / neighbour-stencil library (libtsg.so).
+ *
+ * Drop-in boundary for the hot path of the reference package `tristencil`
+ * (paths below are relative to /root/reference/pkg/src/tristencil).  The reference is
+ * pure Python + numpy and has no FFI, so every entry point here replaces a Python
+ * function; the binding a maintainer would add on the reference side (ctypes) is in
+ * INTEGRATION.md.  Plain pointers and sizes only -- no torch types.
+ *
+ * Conventions
+ *  - Every function returns an int status (TSG_OK = 0).  On failure the message is
+ *    available from tsg_last_error() (thread-local), and the Python wrapper raises the
+ *    reference's exception type with that message (ValueError / IndexError / ...).
+ *  - Device pointers are caller-owned (the library never allocates per call); a
+ *    `tsg_stream` is a cudaStream_t, every launch is stream-ordered and asynchronous.
+ *  - Structured ("direct") fields live in the device layout
+ *        double field[rows + 2][colors][cols + 2][tsg_inner_pitch(inner)]
+ *    i.e. (row, colour, column) parallelogram indexing with a one-element periodic
+ *    halo ring and the level (or extra) axis innermost and contiguous, padded to an
+ *    even count so every element row is 16-byte aligned for TMA / vector access.
+ *    Logical element (i, c, j) sits at storage row i + 1, column j + 1.
+ *  - Flat ("indirect") arrays are row-major [n_elements, n_levels] in any numbering,
+ *    exactly the reference oracle's convention (reference.py:1-11).
+ *  - Locations: 0 = vertices (1 colour), 1 = cells (2 colours), 2 = edges (3 colours)
+ *    (topology.py:27-41).
+ */
+#ifndef TSG_H
+#define TSG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSG_ABI_VERSION 1
+
+typedef struct tsg_grid tsg_grid; /* opaque: patch dims, halo flags, TMA descriptor cache */
+typedef void *tsg_stream;         /* cudaStream_t */
+
+enum tsg_status {
+    TSG_OK = 0,
+    TSG_EVALUE = 1, /* ValueError in the Python mirror */
+    TSG_EINDEX = 2, /* IndexError */
+    TSG_ECUDA = 3,  /* RuntimeError: CUDA / driver failure */
+    TSG_ESTATE = 4  /* RuntimeError: misuse (e.g. no device) */
+};
+
+enum tsg_location { TSG_VERTICES = 0, TSG_CELLS = 1, TSG_EDGES = 2 };
+enum tsg_flux_op { TSG_UPWIND = 0, TSG_CENTRED = 1 };
+enum tsg_grid_flags {
+    TSG_PERIODIC_ROWS = 1, /* single-GPU patch: row halo is a periodic image */
+    TSG_PERIODIC_COLS = 2  /* column halo is a periodic image (always on for row strips) */
+};
+
+/* ---- errors / version ------------------------------------------------------------ */
+const char *tsg_last_error(void);
+int tsg_abi_version(void);
+
+/* ---- grid handle ------------------------------------------------------------------ */
+/* Replaces PatchSpec (topology.py:44-83) on the device side: rows, cols >= 2, levels >= 1.
+ * `flags` = TSG_PERIODIC_ROWS | TSG_PERIODIC_COLS for one patch on one GPU; a row strip
+ * of a multi-GPU decomposition passes TSG_PERIODIC_COLS only (row halos arrive by
+ * exchange).  The handle binds to the current CUDA device. */
+int tsg_grid_create(int rows, int cols, int levels, int flags, tsg_grid **out);
+int tsg_grid_destroy(tsg_grid *g);
+/* Place a row strip inside a global patch of `global_rows` rows (multi-GPU row-strip
+ * decomposition): only tsg_fill_hash consults it, so synthetic inputs are identical for
+ * every decomposition. */
+int tsg_grid_set_origin(tsg_grid *g, int row0, int global_rows);
+/* Padded innermost extent for `inner` contiguous values per element (1 stays 1). */
+int64_t tsg_inner_pitch(int inner);
+/* Number of doubles of a structured field: (rows+2) * colors * (cols+2) * pitch(inner). */
+int64_t tsg_field_elems(const tsg_grid *g, int loc, int inner);
+
+/* ---- field layout: Atlas/flat <-> structured reorder, halo ----------------------- */
+/* Periodic one-ring halo refresh (executors.py:74-86), honouring the grid flags. */
+int tsg_halo_update(const tsg_grid *g, int loc, int inner, double *field, tsg_stream s);
+/* flat[rank, 0..inner) -> structured field (halo images written).  `forward` maps the
+ * canonical id (i*colors + c)*cols + j to the flat row (layouts.Permutation.forward,
+ * layouts.py:153-180); NULL = structured numbering (identity).  Replaces
+ * flat_to_field (kernels.py:120-127) + halo_update. */
+int tsg_pack(const tsg_grid *g, int loc, int inner, const double *flat, const int64_t *forward,
+             double *field, tsg_stream s);
+/* structured field -> flat[rank, 0..inner); replaces field_to_flat (kernels.py:107-117). */
+int tsg_unpack(const tsg_grid *g, int loc, int inner, const double *field,
+               const int64_t *forward, double *flat, tsg_stream s);
+
+/* Host `LinearLayout` buffer (layouts.py:55-104, copied to device memory as is) <->
+ * structured field.  layout6 (host memory) = {front_pad, stride_row, stride_color,
+ * stride_column, stride_level, stride_extra} in elements; the buffer carries a halo of
+ * width host_halo.  `inner` runs along level when stride_level != 0, else along extra.
+ * Unpack writes every host halo cell as the periodic image of the interior. */
+int tsg_pack_strided(const tsg_grid *g, int loc, int inner, const double *src,
+                     const int64_t *layout6, int host_halo, double *field, tsg_stream s);
+int tsg_unpack_strided(const tsg_grid *g, int loc, int inner, const double *field,
+                       const int64_t *layout6, int host_halo, double *dst, tsg_stream s);
+
+/* ---- MPDATA transport step (mpdata.py:189-354; reference.py:93-116) ---------------- */
+/* Fused single-pass step: flux -> fluz -> divergence -> advance with every intermediate
+ * kept on chip (the run_fused executor, executors.py:266-316).  Writes pd_out with its
+ * halo images.  pd, rho, pd_out: vertex fields, inner = levels; vn: edge field,
+ * inner = levels; wn: vertex field, inner = levels + 1 (staggered); signs: vertex field,
+ * inner = 6 (edge_signs, connectivity.py:184-194); dual: vertex field, inner = 1.
+ * Input halos must be valid (tsg_pack / tsg_halo_update / a previous step). */
+int tsg_mpdata_step(tsg_grid *g, const double *pd, const double *vn, const double *wn,
+                    const double *rho, const double *signs, const double *dual, double *pd_out,
+                    double dt, double pivbz, int flux_op, tsg_stream s);
+/* Four-kernel step materialising flux (edges), fluz (vertices, levels+1) and divvd
+ * (vertices) like run_naive (executors.py:213-245), halos refreshed after each stage. */
+int tsg_mpdata_step_unfused(const tsg_grid *g, const double *pd, const double *vn,
+                            const double *wn, const double *rho, const double *signs,
+                            const double *dual, double *flux, double *fluz, double *divvd,
+                            double *pd_out, double dt, double pivbz, int flux_op, tsg_stream s);
+/* Table-driven ("indirect", Atlas-style) step over flat arrays -- the exact signature
+ * of reference.transport_step (reference.py:93-116): e2v [ne,2], v2e [nv,6] int64 ranks,
+ * signs [nv,6], dual [nv], pd/rho/div/pd_out [nv,nlev], vn/flux [ne,nlev],
+ * wn/fluz [nv,nlev+1].  Any numbering. */
+int tsg_transport_indirect(const int64_t *e2v, const int64_t *v2e, const double *signs,
+                           const double *dual, const double *pd, const double *vn,
+                           const double *wn, const double *rho, int64_t nv, int64_t ne,
+                           int nlev, double dt, double pivbz, int flux_op, double *flux,
+                           double *fluz, double *div, double *pd_out, tsg_stream s);
+/* Select the fused kernel's tile variant (0 = auto). Returns the variant in use. */
+int tsg_set_fused_variant(int variant);
+int tsg_fused_variant_info(int variant, int *ti, int *tj, int *kc, int *stages, int *threads,
+                           int *smem_bytes);
+
+/* ---- neighbour reductions (stencil.py:401-408; kernels.py:27-104; reference.py:137-157) */
+/* Structured ("direct") reduce for any of the 9 relations (connectivity.py:36-68):
+ * dst[from, k] = ((0 + src[n0,k]) + src[n1,k]) + ...  (canonical slot order), times
+ * scale[from] if scale != NULL (a 2-D from-located field, inner = 1).  src lives on
+ * to_loc, dst on from_loc, both with `inner` levels; dst halo images are written. */
+int tsg_neighbor_reduce(const tsg_grid *g, int from_loc, int to_loc, int inner,
+                        const double *src, const double *scale, double *dst, tsg_stream s);
+/* Table-driven reduce over flat arrays (Table 1 "indirect access"): table [nrows,width]
+ * int64 ranks into src [*, nlev]; scale [nrows] or NULL; dst [nrows, nlev]. */
+int tsg_neighbor_reduce_indirect(const int64_t *table, int64_t nrows, int width, int nlev,
+                                 const double *src, const double *scale, double *dst,
+                                 tsg_stream s);
+/* Cell divergence demo (mpdata.py:361-416; reference.py:119-134): weighted = 0 computes
+ * (sum vn*length)/area, weighted = 1 computes sum vn*weights[c,n]. vn: edges, inner
+ * levels; length: edges inner 1; area: cells inner 1; weights: cells inner 3. */
+int tsg_cell_divergence(const tsg_grid *g, int weighted, const double *vn,
+                        const double *length, const double *area, const double *weights,
+                        double *out, tsg_stream s);
+
+/* Per-cell edge weights w[c, n] = length(e_n) / area(c) in C->E slot order
+ * (precompute_weights, mpdata.py:152-169): length edges inner 1, area cells inner 1,
+ * weights cells inner 3. */
+int tsg_cell_weights(const tsg_grid *g, const double *length, const double *area,
+                     double *weights, tsg_stream s);
+
+/* ---- index maps on the device (connectivity.py:130-194) ---------------------------- */
+/* Flat int64 neighbour table [n_from, width] under optional numberings:
+ * from_inverse: rank -> canonical id of the from-location (NULL = identity);
+ * to_forward:   canonical id -> rank of the to-location (NULL = identity). */
+int tsg_build_neighbor_table(int rows, int cols, int from_loc, int to_loc,
+                             const int64_t *from_inverse, const int64_t *to_forward,
+                             int64_t *out, tsg_stream s);
+/* Forward permutation (canonical id -> rank) of a numbering (layouts.py:250-279):
+ * numbering 0 = sn (identity), 1 = un ((i*cols + j)*colors + c), 2 = hn (Hilbert walk
+ * over the quad embedding, vertices and cells only).  hn needs `work` with
+ * tsg_permutation_work_elems() int64 entries (may be NULL otherwise). */
+int tsg_make_permutation(int rows, int cols, int loc, int numbering, int64_t *forward,
+                         int64_t *work, tsg_stream s);
+int64_t tsg_permutation_work_elems(int rows, int cols, int loc);
+/* Orientation signs [n_vertices, 6] in canonical order (connectivity.py:184-194). */
+int tsg_edge_signs(int rows, int cols, double *out, tsg_stream s);
+
+/* ---- diagnostics / synthetic inputs ----------------------------------------------- */
+/* sum_v sum_k pd[v,k] * dual[v] (mpdata.py:496-500), deterministic two-pass reduction;
+ * `work` holds >= 1024 doubles; the result is written to device memory `out`. */
+int tsg_total_mass(const tsg_grid *g, const double *pd, const double *dual, double *work,
+                   double *out, tsg_stream s);
+/* Counter-hash uniform values in [lo, hi) for every (element, level), halo images
+ * included -- on-device synthetic inputs for patches the host cannot hold. */
+int tsg_fill_hash(const tsg_grid *g, int loc, int inner, uint64_t seed, double lo, double hi,
+                  double *field, tsg_stream s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSG_H */

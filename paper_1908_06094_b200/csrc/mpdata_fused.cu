@@ -1,0 +1,422 @@
+// Fused MPDATA transport step for sm_100a: one pass over HBM per step.
+//
+// Restates mpdata.py:189-354 (four stages: upwind/centred edge flux, staggered vertical
+// flux with pivbz boundaries, signed divergence over the dual volume, explicit update)
+// with the reference's fused-executor semantics (executors.py:266-316, every
+// intermediate on chip) and its bitwise arithmetic contract.
+//
+// Design (B200):
+//  * Work unit = (TI x TJ vertex tile) x (KC-level chunk).  A persistent grid of
+//    (SMs x resident CTAs) walks a contiguous range of units, so the chunks of one tile
+//    run back to back on one SM (signs/dual stay in registers) and neighbouring tiles
+//    run concurrently (halo re-reads hit L2).
+//  * Per unit, four TMA boxes land in shared memory, STAGES deep, completion tracked by
+//    one mbarrier per stage (expect_tx):
+//       pd  [TI+2][TJ+2][KC+4]  one-ring horizontal halo + levels k0-2 .. k0+KC+1
+//                               (a TMA box must start 16-byte aligned in its inner
+//                               dimension: an even level for fp64)
+//       vn  [TI+1][3][TJ+1][KC] the tile's edges plus the row/column apron edges
+//       wn  [TI][TJ][KC+2]      interfaces k0 .. k0+KC(+1 pad)
+//       rho [TI][TJ][KC]
+//    One elected thread issues the TMA for unit n+STAGES-1 while all threads compute
+//    unit n; __syncthreads() at the end of a unit releases its stage.
+//  * Compute: one thread per (vertex, level), 16 threads per vertex (a half-warp reads a
+//    contiguous 128-byte level run: conflict-free).  Each thread recomputes the six
+//    incident edge fluxes straight from smem (every edge flux is computed by both of its
+//    endpoints -- bitwise identical, no smem round trip, no extra barrier), the two
+//    interface fluxes, the divergence and the update, and stores pd_out (plus periodic
+//    halo images) straight to HBM, coalesced.
+//  * No tensor cores: fp64 stencil, ~0.5 flop/byte, the HBM roofline bounds it.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "tsg_common.cuh"
+
+namespace tsg {
+
+// ---- PTX helpers ----------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0,
+                                            int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0,
+                                            int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+        "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// ---- tile geometry --------------------------------------------------------------------
+
+template <int TI, int TJ, int KC, int STAGES>
+struct FusedCfg {
+    static constexpr int kThreads = TI * TJ * 16;
+    static constexpr int kLevelsPerThread = KC / 16;
+    static constexpr int kPdBytes = (TI + 2) * (TJ + 2) * (KC + 4) * 8;
+    static constexpr int kVnBytes = (TI + 1) * 3 * (TJ + 1) * KC * 8;
+    static constexpr int kWnBytes = TI * TJ * (KC + 2) * 8;
+    static constexpr int kRhoBytes = TI * TJ * KC * 8;
+    static constexpr int align(int b) { return (b + 127) / 128 * 128; }
+    static constexpr int kPdOff = 0;
+    static constexpr int kVnOff = kPdOff + align(kPdBytes);
+    static constexpr int kWnOff = kVnOff + align(kVnBytes);
+    static constexpr int kRhoOff = kWnOff + align(kWnBytes);
+    static constexpr int kStageBytes = kRhoOff + align(kRhoBytes);
+    static constexpr uint32_t kTxBytes = kPdBytes + kVnBytes + kWnBytes + kRhoBytes;
+    static constexpr int kSmemBytes = STAGES * kStageBytes + 128;  // + barriers
+    static_assert(KC % 16 == 0, "KC must be a multiple of 16");
+    static_assert(((KC + 2) * 8) % 16 == 0 && (KC * 8) % 16 == 0, "TMA inner box must be 16B multiple");
+    static_assert(TI + 2 <= 256 && TJ + 2 <= 256 && KC + 4 <= 256, "TMA box <= 256");
+};
+
+struct FusedArgs {
+    const double *signs;  // vertex field, inner 6
+    const double *dual;   // vertex field, inner 1
+    double *pd_out;       // vertex field, inner K
+    int rows, cols, K;
+    int flags;
+    double dt, pivbz;
+    int tiles_j, chunks;
+    int64_t units;
+};
+
+template <int TI, int TJ, int KC, int STAGES, int OP>
+__global__ void __launch_bounds__(TI *TJ * 16)
+    mpdata_fused_kernel(const __grid_constant__ CUtensorMap tm_pd,
+                        const __grid_constant__ CUtensorMap tm_vn,
+                        const __grid_constant__ CUtensorMap tm_wn,
+                        const __grid_constant__ CUtensorMap tm_rho, const FusedArgs a) {
+    using C = FusedCfg<TI, TJ, KC, STAGES>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * C::kStageBytes);
+
+    const int tid = threadIdx.x;
+    const int kl = tid & 15;          // level lane inside the chunk
+    const int vloc = tid >> 4;        // vertex inside the tile
+    const int li = vloc / TJ, lj = vloc % TJ;
+
+    // contiguous unit range of this CTA
+    const int64_t u_begin = a.units * blockIdx.x / gridDim.x;
+    const int64_t u_end = a.units * (blockIdx.x + 1) / gridDim.x;
+    const int n_units = (int)(u_end - u_begin);
+
+    if (tid == 0) {
+        prefetch_tmap(&tm_pd);
+        prefetch_tmap(&tm_vn);
+        prefetch_tmap(&tm_wn);
+        prefetch_tmap(&tm_rho);
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto issue = [&](int64_t u, int stage) {
+        const int chunk = (int)(u % a.chunks);
+        const int64_t tile = u / a.chunks;
+        const int i0 = (int)(tile / a.tiles_j) * TI, j0 = (int)(tile % a.tiles_j) * TJ;
+        const int k0 = chunk * KC;
+        unsigned char *base = smem + stage * C::kStageBytes;
+        uint64_t *bar = &bars[stage];
+        mbar_expect_tx(bar, C::kTxBytes);
+        // storage coordinates: logical (i, j) -> (i + 1, j + 1)
+        tma_load_3d(base + C::kPdOff, &tm_pd, bar, k0 - 2, j0, i0);
+        tma_load_4d(base + C::kVnOff, &tm_vn, bar, k0, j0, 0, i0);
+        tma_load_3d(base + C::kWnOff, &tm_wn, bar, k0, j0 + 1, i0 + 1);
+        tma_load_3d(base + C::kRhoOff, &tm_rho, bar, k0, j0 + 1, i0 + 1);
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES - 1 && s < n_units; ++s) issue(u_begin + s, s);
+    }
+
+    const FieldIx Fv(a.rows, a.cols, 1, a.K), Fs(a.rows, a.cols, 1, 6), Fd(a.rows, a.cols, 1, 1);
+    int64_t cur_tile = -1;
+    double sg0 = 0, sg1 = 0, sg2 = 0, sg3 = 0, sg4 = 0, sg5 = 0, dual = 1.0;
+
+    for (int n = 0; n < n_units; ++n) {
+        const int stage = n % STAGES;
+        if (tid == 0 && n + STAGES - 1 < n_units) {
+            // that stage was released by the __syncthreads() closing unit n-1
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(u_begin + n + STAGES - 1, (n + STAGES - 1) % STAGES);
+        }
+        const int64_t u = u_begin + n;
+        const int chunk = (int)(u % a.chunks);
+        const int64_t tile = u / a.chunks;
+        const int i = (int)(tile / a.tiles_j) * TI + li;
+        const int j = (int)(tile % a.tiles_j) * TJ + lj;
+        const bool vvalid = i < a.rows && j < a.cols;
+        if (tile != cur_tile) {
+            cur_tile = tile;
+            if (vvalid) {
+                const double *S = a.signs + Fs.at(i, 0, j);
+                sg0 = __ldg(S + 0); sg1 = __ldg(S + 1); sg2 = __ldg(S + 2);
+                sg3 = __ldg(S + 3); sg4 = __ldg(S + 4); sg5 = __ldg(S + 5);
+                dual = __ldg(a.dual + Fd.at(i, 0, j));
+            }
+        }
+
+        mbar_wait(&bars[stage], (uint32_t)((n / STAGES) & 1));
+
+        const unsigned char *base = smem + stage * C::kStageBytes;
+        const double *sp = reinterpret_cast<const double *>(base + C::kPdOff);
+        const double *sv = reinterpret_cast<const double *>(base + C::kVnOff);
+        const double *sw = reinterpret_cast<const double *>(base + C::kWnOff);
+        const double *sr = reinterpret_cast<const double *>(base + C::kRhoOff);
+
+#pragma unroll
+        for (int h = 0; h < C::kLevelsPerThread; ++h) {
+            const int kk = kl + 16 * h;  // level inside the chunk
+            const int k = chunk * KC + kk;
+            if (vvalid && k < a.K) {
+                // pd box: [TI+2][TJ+2][KC+4], origin (i0-1, j0-1, k0-2)
+                auto P = [&](int di, int dj, int dk) -> double {
+                    return sp[((li + 1 + di) * (TJ + 2) + (lj + 1 + dj)) * (KC + 4) + (kk + 2 + dk)];
+                };
+                // vn box: [TI+1][3][TJ+1][KC], origin (i0-1, colour 0, j0-1, k0)
+                auto VN = [&](int c, int di, int dj) -> double {
+                    return sv[(((li + 1 + di) * 3 + c) * (TJ + 1) + (lj + 1 + dj)) * KC + kk];
+                };
+                const double p0 = P(0, 0, 0);
+                // the six incident edges in V->E slot order (connectivity.py:66); the
+                // origin is E->V slot 0 (connectivity.py:38-42)
+                const double f0 = edge_flux<OP>(p0, P(0, 1, 0), VN(0, 0, 0));
+                const double f1 = edge_flux<OP>(p0, P(1, 1, 0), VN(1, 0, 0));
+                const double f2 = edge_flux<OP>(p0, P(1, 0, 0), VN(2, 0, 0));
+                const double f3 = edge_flux<OP>(P(0, -1, 0), p0, VN(0, 0, -1));
+                const double f4 = edge_flux<OP>(P(-1, -1, 0), p0, VN(1, -1, -1));
+                const double f5 = edge_flux<OP>(P(-1, 0, 0), p0, VN(2, -1, 0));
+                // interface fluxes fluz(k), fluz(k+1) (reference.py:38-60)
+                const double *W = sw + (li * TJ + lj) * (KC + 2) + kk;  // W[0] = wn(k)
+                double fz_lo = fluz_interior(W[0], P(0, 0, -1), p0);
+                double fz_hi = fluz_interior(W[1], p0, P(0, 0, 1));
+                if (k == 0) fz_lo = mul(a.pivbz, fz_hi);
+                if (k == a.K - 1) fz_hi = mul(a.pivbz, fz_lo);
+                // signed divergence (reference.py:63-79), canonical slot order from 0.0
+                double acc = 0.0;
+                acc = add(mul(sg0, f0), acc);
+                acc = add(mul(sg1, f1), acc);
+                acc = add(mul(sg2, f2), acc);
+                acc = add(mul(sg3, f3), acc);
+                acc = add(mul(sg4, f4), acc);
+                acc = add(mul(sg5, f5), acc);
+                acc = add(acc, sub(fz_hi, fz_lo));
+                const double div = dvd(acc, dual);
+                // explicit update (reference.py:82-90)
+                double slope = mul(a.dt, div);
+                slope = dvd(slope, sr[(li * TJ + lj) * KC + kk]);
+                store_img(a.pd_out, Fv, i, 0, j, k, sub(p0, slope), a.flags);
+            }
+        }
+        __syncthreads();  // every thread is done with this stage
+    }
+}
+
+// ---- host side ------------------------------------------------------------------------
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
+
+static int get_encode() {
+    std::call_once(g_encode_once, [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    });
+    if (!g_encode) return fail(TSG_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    return TSG_OK;
+}
+
+static int make_map(CUtensorMap *m, const double *ptr, int rank, const cuuint64_t *dims,
+                    const cuuint64_t *strides_bytes, const cuuint32_t *box) {
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (reinterpret_cast<uintptr_t>(ptr) % 16)
+        return fail(TSG_EVALUE, "field base address must be 16-byte aligned for TMA");
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double *>(ptr), dims,
+                          strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(TSG_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return TSG_OK;
+}
+
+struct Variant {
+    int ti, tj, kc, stages;
+    int threads, smem;
+    void *fn[2];  // upwind, centred
+};
+
+template <int TI, int TJ, int KC, int STAGES>
+static Variant make_variant() {
+    using C = FusedCfg<TI, TJ, KC, STAGES>;
+    Variant v;
+    v.ti = TI;
+    v.tj = TJ;
+    v.kc = KC;
+    v.stages = STAGES;
+    v.threads = C::kThreads;
+    v.smem = C::kSmemBytes;
+    v.fn[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, TSG_UPWIND>;
+    v.fn[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, TSG_CENTRED>;
+    return v;
+}
+
+static Variant *variants(int *count) {
+    static Variant v[] = {
+        make_variant<4, 16, 16, 3>(),  // 1: 1024 threads, 3 x 65.5 KB
+        make_variant<4, 8, 16, 3>(),   // 2: 512 threads, 2 CTAs/SM
+        make_variant<8, 8, 16, 3>(),   // 3: 1024 threads, 3 x 62.9 KB
+        make_variant<2, 16, 32, 3>(),  // 4: 512 threads, 2 levels/thread
+        make_variant<4, 8, 16, 5>(),   // 5: 512 threads, 1 CTA/SM, 5 stages
+    };
+    *count = (int)(sizeof(v) / sizeof(v[0]));
+    return v;
+}
+
+static int g_variant = 1;
+
+}  // namespace tsg
+
+using namespace tsg;
+
+extern "C" int tsg_set_fused_variant(int variant) {
+    int n = 0;
+    variants(&n);
+    if (variant < 0 || variant > n) return fail(TSG_EVALUE, "fused variant must be in [0, %d]", n);
+    g_variant = variant == 0 ? 1 : variant;
+    return g_variant;
+}
+
+extern "C" int tsg_fused_variant_info(int variant, int *ti, int *tj, int *kc, int *stages,
+                                      int *threads, int *smem_bytes) {
+    int n = 0;
+    Variant *vs = variants(&n);
+    if (variant == 0) variant = g_variant;
+    if (variant < 1 || variant > n) return fail(TSG_EVALUE, "fused variant must be in [1, %d]", n);
+    const Variant &v = vs[variant - 1];
+    if (ti) *ti = v.ti;
+    if (tj) *tj = v.tj;
+    if (kc) *kc = v.kc;
+    if (stages) *stages = v.stages;
+    if (threads) *threads = v.threads;
+    if (smem_bytes) *smem_bytes = v.smem;
+    return TSG_OK;
+}
+
+extern "C" int tsg_mpdata_step(tsg_grid *g, const double *pd, const double *vn, const double *wn,
+                               const double *rho, const double *signs, const double *dual,
+                               double *pd_out, double dt, double pivbz, int flux_op, tsg_stream s) {
+    if (!g) return fail(TSG_EVALUE, "grid is NULL");
+    const int K = g->levels;
+    if (K < 2) return fail(TSG_EVALUE, "the transport step needs at least 2 levels, got %d", K);
+    if (flux_op != TSG_UPWIND && flux_op != TSG_CENTRED)
+        return fail(TSG_EVALUE, "flux operator must be one of ['centred', 'upwind'], got %d", flux_op);
+    if (!pd || !vn || !wn || !rho || !signs || !dual || !pd_out)
+        return fail(TSG_EVALUE, "tsg_mpdata_step: NULL array");
+    if (pd_out == pd) return fail(TSG_EVALUE, "pd_out must not alias pd (double-buffer the density)");
+    if (int rc = get_encode()) return rc;
+
+    int n = 0;
+    Variant *vs = variants(&n);
+    const Variant &v = vs[g_variant - 1];
+
+    const int rows = g->rows, cols = g->cols;
+    const cuuint64_t pv = (cuuint64_t)pitch_of(K), pw = (cuuint64_t)pitch_of(K + 1);
+    const cuuint64_t W = (cuuint64_t)cols + 2, H = (cuuint64_t)rows + 2;
+    CUtensorMap m_pd, m_vn, m_wn, m_rho;
+    {
+        cuuint64_t dims[3] = {pv, W, H};
+        cuuint64_t str[2] = {pv * 8, W * pv * 8};
+        cuuint32_t box[3] = {(cuuint32_t)v.kc + 4, (cuuint32_t)v.tj + 2, (cuuint32_t)v.ti + 2};
+        if (int rc = make_map(&m_pd, pd, 3, dims, str, box)) return rc;
+        cuuint32_t boxr[3] = {(cuuint32_t)v.kc, (cuuint32_t)v.tj, (cuuint32_t)v.ti};
+        if (int rc = make_map(&m_rho, rho, 3, dims, str, boxr)) return rc;
+    }
+    {
+        cuuint64_t dims[4] = {pv, W, 3, H};
+        cuuint64_t str[3] = {pv * 8, W * pv * 8, 3 * W * pv * 8};
+        cuuint32_t box[4] = {(cuuint32_t)v.kc, (cuuint32_t)v.tj + 1, 3, (cuuint32_t)v.ti + 1};
+        if (int rc = make_map(&m_vn, vn, 4, dims, str, box)) return rc;
+    }
+    {
+        cuuint64_t dims[3] = {pw, W, H};
+        cuuint64_t str[2] = {pw * 8, W * pw * 8};
+        cuuint32_t box[3] = {(cuuint32_t)v.kc + 2, (cuuint32_t)v.tj, (cuuint32_t)v.ti};
+        if (int rc = make_map(&m_wn, wn, 3, dims, str, box)) return rc;
+    }
+
+    FusedArgs a;
+    a.signs = signs;
+    a.dual = dual;
+    a.pd_out = pd_out;
+    a.rows = rows;
+    a.cols = cols;
+    a.K = K;
+    a.flags = g->flags;
+    a.dt = dt;
+    a.pivbz = pivbz;
+    const int tiles_i = (rows + v.ti - 1) / v.ti;
+    a.tiles_j = (cols + v.tj - 1) / v.tj;
+    a.chunks = (K + v.kc - 1) / v.kc;
+    a.units = (int64_t)tiles_i * a.tiles_j * a.chunks;
+
+    void *fn = v.fn[flux_op];
+    TSG_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
+    int per_sm = 0;
+    TSG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, v.threads, v.smem));
+    if (per_sm < 1) return fail(TSG_ECUDA, "fused variant %d does not fit on an SM", g_variant);
+    int64_t grid = (int64_t)g->num_sms * per_sm;
+    if (grid > a.units) grid = a.units;
+
+    void *args[] = {&m_pd, &m_vn, &m_wn, &m_rho, &a};
+    TSG_CHECK_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(v.threads), args, v.smem,
+                                    (cudaStream_t)s));
+    return TSG_OK;
+}

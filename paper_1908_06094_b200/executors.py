@@ -1,0 +1,208 @@
+"""GPU runners behind the reference's executor protocol ``runner(comp) -> RunStats``.
+
+The reference runs stage bodies through ``run_naive`` / ``run_fused``
+(executors.py:213-316); time_computation takes any such runner
+(executors.py:390-414).  Here:
+
+* :func:`run_gpu` executes a computation on the device.  ``fused=True`` is the
+  single-pass TMA kernel (``tsg_mpdata_step``); ``fused=False`` is the
+  four-kernel path that materialises flux / fluz / divvd like ``run_naive``.
+* :func:`run_naive` / :func:`run_fused` keep the reference's signatures so
+  existing call sites work unchanged (``TileSpec`` is validated and recorded;
+  the device tiling is the kernel's own).
+
+Inputs are uploaded on demand (primary -> mirror, reordered on the GPU);
+outputs are written on the device and, with ``download=True`` (default, the
+reference's semantics: results are readable from the Field afterwards),
+synced back to the host.  ``download=False`` leaves them device-resident.
+"""
+
+from __future__ import annotations
+
+import statistics
+import time
+from dataclasses import dataclass, field as dc_field
+
+from . import _lib
+from .storage import Field, device_grid, sync
+
+_FLUX_CODE = {"upwind": 0, "centred": 1}
+
+
+@dataclass(frozen=True)
+class TileSpec:
+    tile_i: int
+    tile_j: int
+    workers: int = 1
+
+    def __post_init__(self):
+        if self.tile_i < 1 or self.tile_j < 1:
+            raise ValueError(f"tile sizes must be >= 1, got {self.tile_i}x{self.tile_j}")
+        if self.workers < 1:
+            raise ValueError(f"workers must be >= 1, got {self.workers}")
+
+
+@dataclass
+class RunStats:
+    """Device times and update counts of one run (executors.py:48-71).
+
+    ``wall_times`` holds the CUDA-event device time of the launch sequence in
+    seconds; ``traffic()`` reports the algorithmic bytes of the step.
+    """
+
+    tag: str
+    executor: str
+    fields: list = dc_field(default_factory=list)
+    wall_times: dict = dc_field(default_factory=dict)
+    stage_updates: dict = dc_field(default_factory=dict)
+    bytes_moved: int = 0
+
+    @property
+    def total_wall(self) -> float:
+        return sum(self.wall_times.values())
+
+    @property
+    def total_updates(self) -> int:
+        return sum(self.stage_updates.values())
+
+    def traffic(self) -> dict:
+        return {"algorithmic_bytes": self.bytes_moved}
+
+
+def halo_update(field: Field, space: str = "primary") -> None:
+    """Refresh the periodic halo (executors.py:74-86); 'mirror' runs tsg_halo_update."""
+    if space == "mirror":
+        grid = device_grid(field.spec)
+        t = field.buffer("mirror")
+        _lib.call("tsg_halo_update", grid.handle, field.loc_code, field.inner, _lib.ptr(t),
+                  _lib.stream_handle())
+        field.dirty["mirror"] = True
+        return
+    spec = field.spec
+    h, rows, cols = spec.halo, spec.rows, spec.cols
+    arr = field.array(space, "rw")
+    arr[:h] = arr[rows:rows + h]
+    arr[h + rows:] = arr[h:2 * h]
+    arr[:, :, :h] = arr[:, :, cols:cols + h]
+    arr[:, :, h + cols:] = arr[:, :, h:2 * h]
+
+
+def mpdata_bytes(rows: int, cols: int, levels: int, fused: bool = True) -> int:
+    """Algorithmic HBM bytes of one step (SURVEY 8(d) B_comp; unfused: DISTINCT model)."""
+    v, e = rows * cols, 3 * rows * cols
+    if fused:
+        return 8 * (v * levels + e * levels + v * (levels - 1) + v * levels + v * levels)
+    # flux: pd r, vn r, flux w; fluz: pd r, wn r, fluz w; div: flux r, fluz r, div w;
+    # advance: pd r, div r, rho r, pd_out w
+    return 8 * (3 * e * levels + 7 * v * levels + 2 * v * (levels + 1) + v * (levels - 1))
+
+
+def _launch(comp, fused: bool, stream):
+    import torch
+
+    grid = device_grid(comp.patch)
+    s = _lib.stream_handle(stream)
+    if comp.kind == "mpdata":
+        st, geo, p = comp.state, comp.geo, comp.params
+        ins = [st.pd_in.ensure_device(), st.vn.ensure_device(), st.wn.ensure_device(),
+               st.rho.ensure_device(), geo.edge_signs.ensure_device(),
+               geo.dual_volumes.ensure_device()]
+        outs = [st.pd_out] if fused else [st.flux, st.fluz, st.divvd, st.pd_out]
+        optrs = [_lib.ptr(f.buffer("mirror")) for f in outs]
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        if fused:
+            _lib.call("tsg_mpdata_step", grid.handle, *[_lib.ptr(t) for t in ins], *optrs,
+                      float(p.dt), float(p.pivbz), _FLUX_CODE[comp.flux_op], s)
+        else:
+            _lib.call("tsg_mpdata_step_unfused", grid.handle, *[_lib.ptr(t) for t in ins], *optrs,
+                      float(p.dt), float(p.pivbz), _FLUX_CODE[comp.flux_op], s)
+        end.record(stream)
+        nbytes = mpdata_bytes(comp.patch.rows, comp.patch.cols, comp.patch.levels, fused)
+    elif comp.kind == "divergence":
+        g = comp.geo
+        vn = comp.state.vn.ensure_device()
+        if comp.weighted:
+            length = area = None
+            w = g.weights.ensure_device()
+        else:
+            length, area, w = g.edge_length.ensure_device(), g.cell_area.ensure_device(), None
+        outs = [comp.out]
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        _lib.call("tsg_cell_divergence", grid.handle, int(comp.weighted), _lib.ptr(vn),
+                  _lib.ptr(length), _lib.ptr(area), _lib.ptr(w),
+                  _lib.ptr(comp.out.buffer("mirror")), s)
+        end.record(stream)
+        nbytes = 8 * comp.patch.rows * comp.patch.cols * comp.patch.levels * 5
+    elif comp.kind == "reduce":
+        src = comp.src.ensure_device()
+        scale = comp.scale.ensure_device() if comp.scale is not None else None
+        outs = [comp.dst]
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        _lib.call("tsg_neighbor_reduce", grid.handle, comp.from_loc.code, comp.to_loc.code,
+                  comp.dst.inner, _lib.ptr(src), _lib.ptr(scale),
+                  _lib.ptr(comp.dst.buffer("mirror")), s)
+        end.record(stream)
+        nbytes = comp.algorithmic_bytes()
+    else:
+        raise TypeError(f"cannot run computation of kind {getattr(comp, 'kind', None)!r}")
+    for f in outs:
+        f.mark_device_written()
+    return outs, (start, end), nbytes
+
+
+def run_gpu(comp, fused: bool = True, run_tag: str = "gpu", download: bool = True,
+            stream=None) -> RunStats:
+    """Execute ``comp`` on the current CUDA device; returns RunStats."""
+    outs, (start, end), nbytes = _launch(comp, fused, stream)
+    end.synchronize()
+    stats = RunStats(tag=run_tag, executor="gpu-fused" if fused else "gpu-unfused",
+                     fields=comp.fields(), stage_updates=comp.stage_updates(), bytes_moved=nbytes)
+    stats.wall_times["ms0"] = start.elapsed_time(end) / 1e3
+    if download:
+        for f in outs:
+            sync(f, "primary")
+    return stats
+
+
+def run_naive(comp, run_tag: str = "naive") -> RunStats:
+    """Stage-by-stage device execution materialising every intermediate (executors.py:213)."""
+    return run_gpu(comp, fused=comp.kind != "mpdata", run_tag=run_tag)
+
+
+def run_fused(comp, tiles: TileSpec | None = None, run_tag: str = "fused") -> RunStats:
+    """Single-pass fused device execution (executors.py:266); tiles are the kernel's own."""
+    if tiles is not None and not isinstance(tiles, TileSpec):
+        raise TypeError("tiles must be a TileSpec")
+    return run_gpu(comp, fused=True, run_tag=run_tag)
+
+
+@dataclass
+class TimingResult:
+    median_seconds: float
+    seconds_per_update: float
+    times: list
+    updates: int
+
+
+def time_computation(comp, runner, reps: int = 10, warmup: int = 1) -> TimingResult:
+    """Median wall time of ``runner(comp)`` (device work included) after warm-up."""
+    import torch
+
+    if reps < 1:
+        raise ValueError(f"reps must be >= 1, got {reps}")
+    stats = None
+    for _ in range(warmup):
+        stats = runner(comp)
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        stats = runner(comp)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    updates = stats.total_updates
+    median = statistics.median(times)
+    return TimingResult(median, median / updates if updates else float("nan"), times, updates)

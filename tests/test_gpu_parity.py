@@ -1,0 +1,116 @@
+"""GPU parity: every CUDA path against the reference's golden vectors / the oracle.
+
+All comparisons are bitwise (np.array_equal / SHA-256 of the float64 bytes),
+stricter than the north-star tolerance (fp64 within 1e-12 relative); index
+maps are bit-exact by construction of the test.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import tsg_oracle as O
+from tests.gpu_helpers import fused_step, golden_inputs, oracle_tables, unfused_step
+from tests.hashing import sha
+
+pytestmark = pytest.mark.gpu
+
+LOCS = {"vertices": 0, "cells": 1, "edges": 2}
+
+
+def test_device_tables_and_signs(cuda_ok, golden):
+    import paper_1908_06094_b200 as T
+
+    for r, c in ((2, 2), (3, 3), (2, 5), (4, 3), (5, 6), (7, 4), (8, 8)):
+        spec = T.PatchSpec(r, c, 1)
+        for (f, t) in T.OFFSET_TABLES:
+            got = T.build_neighbor_table(spec, f, t).ids
+            assert np.array_equal(got, golden[f"tbl_{r}x{c}_{f.value}_{t.value}"]), (r, c, f, t)
+        assert np.array_equal(T.edge_signs_table(spec), golden[f"signs_{r}x{c}"])
+
+
+def test_device_numberings(cuda_ok, golden):
+    import paper_1908_06094_b200 as T
+
+    for r, c in ((5, 7), (16, 8), (3, 9), (4, 4), (4, 2), (6, 5)):
+        spec = T.PatchSpec(r, c, 1)
+        for loc in T.LocationType:
+            p = T.make_permutation(T.Numbering.UN, spec, loc)
+            assert np.array_equal(p.forward, golden[f"perm_un_{r}x{c}_{loc.value}"])
+        for loc in (T.LocationType.VERTICES, T.LocationType.CELLS):
+            p = T.make_permutation(T.Numbering.HN, spec, loc)
+            assert np.array_equal(p.forward, golden[f"perm_hn_{r}x{c}_{loc.value}"])
+    spec = T.PatchSpec(4, 4, 1)
+    pv = T.make_permutation(T.Numbering.HN, spec, T.LocationType.VERTICES)
+    pe = T.make_permutation(T.Numbering.UN, spec, T.LocationType.EDGES)
+    got = T.build_neighbor_table(spec, T.LocationType.EDGES, T.LocationType.VERTICES, pe, pv).ids
+    assert np.array_equal(got, golden["tblp_relabel_4x4_edges_vertices"])
+    got = T.build_neighbor_table(spec, T.LocationType.VERTICES, T.LocationType.EDGES, pv, pe).ids
+    assert np.array_equal(got, golden["tblp_relabel_4x4_vertices_edges"])
+
+
+def test_fused_step_small_cases(cuda_ok, golden, golden_hashes):
+    for meta in golden_hashes["small_transport"]:
+        k = meta["key"]
+        r, c, lev = meta["shape"]
+        got = fused_step(r, c, lev, golden_inputs(golden, k), meta["dt"], meta["pivbz"], meta["flux_op"])
+        assert np.array_equal(got, golden[f"{k}_pd_out"]), k
+
+
+def test_unfused_step_small_cases(cuda_ok, golden, golden_hashes):
+    for meta in golden_hashes["small_transport"]:
+        k = meta["key"]
+        r, c, lev = meta["shape"]
+        got = unfused_step(r, c, lev, golden_inputs(golden, k), meta["dt"], meta["pivbz"], meta["flux_op"])
+        for name in ("flux", "fluz", "div", "pd_out"):
+            assert np.array_equal(got[name], golden[f"{k}_{name}"]), (k, name)
+
+
+def test_indirect_step_small_cases(cuda_ok, golden, golden_hashes):
+    from paper_1908_06094_b200 import transport_step
+
+    for meta in golden_hashes["small_transport"]:
+        k = meta["key"]
+        r, c, _ = meta["shape"]
+        e2v, v2e = oracle_tables(r, c)
+        inp = golden_inputs(golden, k)
+        out = transport_step(e2v, v2e, inp["signs"], inp["dual"], inp["pd"], inp["vn"], inp["wn"],
+                             inp["rho"], meta["dt"], meta["pivbz"], meta["flux_op"])
+        for name in ("flux", "fluz", "div", "pd_out"):
+            assert np.array_equal(out[name], golden[f"{k}_{name}"]), (k, name)
+
+
+@pytest.mark.parametrize("key", ["cfg1_s0", "cfg1_s1", "cfg1_default", "cfg2_rand", "cfg3_rand",
+                                 "cfg3_default"])
+def test_fused_step_bench_sizes_match_reference_hash(cuda_ok, golden_hashes, key):
+    e = golden_hashes["transport"][key]
+    cfg = e["config"]
+    inp = O.transport_inputs(e["rows"], e["cols"], e["levels"], cfg.get("seed", 0),
+                             cfg.get("geometry", "uniform"), cfg.get("preset", "gaussian-bump"), "one")
+    if e["exp_dependent"] and sha(inp["pd"]) != e["inputs"]["pd"]:
+        # this host's np.exp differs in the last ulp: compare against the oracle instead
+        want = sha(O.step_inputs(e["rows"], e["cols"], inp, e["dt"], e["pivbz"])["pd_out"])
+    else:
+        assert {n: sha(inp[n]) for n in e["inputs"]} == e["inputs"]
+        want = e["outputs"]["pd_out"]
+    got = fused_step(e["rows"], e["cols"], e["levels"], inp, e["dt"], e["pivbz"])
+    assert sha(got) == want
+
+
+def test_unfused_bench_size_matches_reference_hash(cuda_ok, golden_hashes):
+    e = golden_hashes["transport"]["cfg2_rand"]
+    inp = O.transport_inputs(128, 128, 80, 0, "random", "random", "one")
+    got = unfused_step(128, 128, 80, inp, e["dt"], e["pivbz"])
+    assert {n: sha(got[n]) for n in e["outputs"]} == e["outputs"]
+
+
+def test_multistep_time_loop_matches_reference_hash(cuda_ok, golden_hashes):
+    from tests.gpu_helpers import stepper_for
+
+    e = golden_hashes["transport"]["cfg1_s2_10steps"]
+    inp = O.transport_inputs(44, 72, 10, 2, "random", "random", "one")
+    st = stepper_for(44, 72, 10, inp)
+    for _ in range(e["steps"]):
+        st.step(e["dt"], e["pivbz"])
+        st.swap()
+    st.swap()
+    assert sha(st.download()) == e["outputs"]["pd_out"]
