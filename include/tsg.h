@@ -120,7 +120,7 @@ int tsg_transport_indirect(const int64_t *e2v, const int64_t *v2e, const double 
                            const double *wn, const double *rho, int64_t nv, int64_t ne,
                            int nlev, double dt, double pivbz, int flux_op, double *flux,
                            double *fluz, double *div, double *pd_out, tsg_stream s);
-/* Select the fused kernel's tile variant (0 = auto). Returns the variant in use. */
+/* Select the fused kernel's tile variant (0 = default); variant 0 in _info = current. */
 int tsg_set_fused_variant(int variant);
 int tsg_fused_variant_info(int variant, int *ti, int *tj, int *kc, int *stages, int *threads,
                            int *smem_bytes);

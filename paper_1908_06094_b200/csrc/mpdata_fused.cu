@@ -135,14 +135,24 @@ __global__ void __launch_bounds__(TI *TJ * 16)
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * C::kStageBytes);
 
     const int tid = threadIdx.x;
-    const int kl = tid & 15;          // level lane inside the chunk
-    const int vloc = tid >> 4;        // vertex inside the tile
+    const int kl = tid & 15;    // level lane inside the chunk
+    const int vloc = tid >> 4;  // vertex inside the tile
     const int li = vloc / TJ, lj = vloc % TJ;
 
-    // contiguous unit range of this CTA
-    const int64_t u_begin = a.units * blockIdx.x / gridDim.x;
-    const int64_t u_end = a.units * (blockIdx.x + 1) / gridDim.x;
-    const int n_units = (int)(u_end - u_begin);
+    // Stage-relative smem offsets (doubles) of this thread's point; fixed for the kernel.
+    // pd box [TI+2][TJ+2][KC+4] with origin (i0-1, j0-1, k0-2)
+    constexpr int sPj = KC + 4, sPi = (TJ + 2) * (KC + 4);
+    // vn box [TI+1][3][TJ+1][KC] with origin (i0-1, colour 0, j0-1, k0)
+    constexpr int sVc = (TJ + 1) * KC, sVi = 3 * (TJ + 1) * KC;
+    const int oP = (li + 1) * sPi + (lj + 1) * sPj + kl + 2;
+    const int oV = (li + 1) * sVi + (lj + 1) * KC + kl;
+    const int oW = (li * TJ + lj) * (KC + 2) + kl;
+    const int oR = (li * TJ + lj) * KC + kl;
+
+    // contiguous unit range of this CTA; unit = tile * chunks + chunk (tile-major)
+    const int u_begin = (int)(a.units * blockIdx.x / gridDim.x);
+    const int u_end = (int)(a.units * (blockIdx.x + 1) / gridDim.x);
+    const int n_units = u_end - u_begin;
 
     if (tid == 0) {
         prefetch_tmap(&tm_pd);
@@ -154,11 +164,11 @@ __global__ void __launch_bounds__(TI *TJ * 16)
     }
     __syncthreads();
 
-    auto issue = [&](int64_t u, int stage) {
-        const int chunk = (int)(u % a.chunks);
-        const int64_t tile = u / a.chunks;
-        const int i0 = (int)(tile / a.tiles_j) * TI, j0 = (int)(tile % a.tiles_j) * TJ;
-        const int k0 = chunk * KC;
+    // producer cursor (thread 0 only), decoded once, then advanced incrementally
+    int p_chunk = u_begin % a.chunks, p_tile = u_begin / a.chunks;
+    int p_ti = p_tile / a.tiles_j, p_tj = p_tile % a.tiles_j;
+    auto issue_next = [&](int stage) {
+        const int i0 = p_ti * TI, j0 = p_tj * TJ, k0 = p_chunk * KC;
         unsigned char *base = smem + stage * C::kStageBytes;
         uint64_t *bar = &bars[stage];
         mbar_expect_tx(bar, C::kTxBytes);
@@ -167,75 +177,90 @@ __global__ void __launch_bounds__(TI *TJ * 16)
         tma_load_4d(base + C::kVnOff, &tm_vn, bar, k0, j0, 0, i0);
         tma_load_3d(base + C::kWnOff, &tm_wn, bar, k0, j0 + 1, i0 + 1);
         tma_load_3d(base + C::kRhoOff, &tm_rho, bar, k0, j0 + 1, i0 + 1);
+        if (++p_chunk == a.chunks) {
+            p_chunk = 0;
+            if (++p_tj == a.tiles_j) {
+                p_tj = 0;
+                ++p_ti;
+            }
+        }
     };
-
     if (tid == 0) {
-        for (int s = 0; s < STAGES - 1 && s < n_units; ++s) issue(u_begin + s, s);
+        for (int s = 0; s < STAGES - 1 && s < n_units; ++s) issue_next(s);
     }
 
-    const FieldIx Fv(a.rows, a.cols, 1, a.K), Fs(a.rows, a.cols, 1, 6), Fd(a.rows, a.cols, 1, 1);
-    int64_t cur_tile = -1;
+    // consumer cursor
+    int chunk = u_begin % a.chunks, tile = u_begin / a.chunks;
+    int ti = tile / a.tiles_j, tj = tile % a.tiles_j;
+    const int64_t pv = pitch_of(a.K), rowstride = (int64_t)(a.cols + 2) * pv;
+    const int last_chunk = a.chunks - 1;
+
+    // per-tile thread state (refreshed when a new tile starts)
+    bool vvalid = false;
     double sg0 = 0, sg1 = 0, sg2 = 0, sg3 = 0, sg4 = 0, sg5 = 0, dual = 1.0;
+    double *out = nullptr;
+    int64_t d_row = 0, d_col = 0;  // offsets of the periodic halo images (0 = none)
 
     for (int n = 0; n < n_units; ++n) {
         const int stage = n % STAGES;
         if (tid == 0 && n + STAGES - 1 < n_units) {
             // that stage was released by the __syncthreads() closing unit n-1
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(u_begin + n + STAGES - 1, (n + STAGES - 1) % STAGES);
+            issue_next((n + STAGES - 1) % STAGES);
         }
-        const int64_t u = u_begin + n;
-        const int chunk = (int)(u % a.chunks);
-        const int64_t tile = u / a.chunks;
-        const int i = (int)(tile / a.tiles_j) * TI + li;
-        const int j = (int)(tile % a.tiles_j) * TJ + lj;
-        const bool vvalid = i < a.rows && j < a.cols;
-        if (tile != cur_tile) {
-            cur_tile = tile;
+        if (n == 0 || chunk == 0) {
+            const int i = ti * TI + li, j = tj * TJ + lj;
+            vvalid = i < a.rows && j < a.cols;
             if (vvalid) {
-                const double *S = a.signs + Fs.at(i, 0, j);
+                const int64_t cell = (int64_t)(i + 1) * (a.cols + 2) + (j + 1);
+                const double *S = a.signs + cell * 6;
                 sg0 = __ldg(S + 0); sg1 = __ldg(S + 1); sg2 = __ldg(S + 2);
                 sg3 = __ldg(S + 3); sg4 = __ldg(S + 4); sg5 = __ldg(S + 5);
-                dual = __ldg(a.dual + Fd.at(i, 0, j));
+                dual = __ldg(a.dual + cell);
+                out = a.pd_out + cell * pv;
+                d_row = 0;
+                d_col = 0;
+                if (a.flags & TSG_PERIODIC_ROWS) {
+                    if (i == 0) d_row = (int64_t)a.rows * rowstride;
+                    else if (i == a.rows - 1) d_row = -(int64_t)a.rows * rowstride;
+                }
+                if (a.flags & TSG_PERIODIC_COLS) {
+                    if (j == 0) d_col = (int64_t)a.cols * pv;
+                    else if (j == a.cols - 1) d_col = -(int64_t)a.cols * pv;
+                }
             }
         }
 
         mbar_wait(&bars[stage], (uint32_t)((n / STAGES) & 1));
 
-        const unsigned char *base = smem + stage * C::kStageBytes;
-        const double *sp = reinterpret_cast<const double *>(base + C::kPdOff);
-        const double *sv = reinterpret_cast<const double *>(base + C::kVnOff);
-        const double *sw = reinterpret_cast<const double *>(base + C::kWnOff);
-        const double *sr = reinterpret_cast<const double *>(base + C::kRhoOff);
+        const double *sp = reinterpret_cast<const double *>(smem + stage * C::kStageBytes + C::kPdOff) + oP;
+        const double *sv = reinterpret_cast<const double *>(smem + stage * C::kStageBytes + C::kVnOff) + oV;
+        const double *sw = reinterpret_cast<const double *>(smem + stage * C::kStageBytes + C::kWnOff) + oW;
+        const double *sr = reinterpret_cast<const double *>(smem + stage * C::kStageBytes + C::kRhoOff) + oR;
+        const int k0 = chunk * KC;
 
 #pragma unroll
         for (int h = 0; h < C::kLevelsPerThread; ++h) {
-            const int kk = kl + 16 * h;  // level inside the chunk
-            const int k = chunk * KC + kk;
+            const int kk = 16 * h;  // level offset of this pass inside the chunk
+            const int k = k0 + kl + kk;
             if (vvalid && k < a.K) {
-                // pd box: [TI+2][TJ+2][KC+4], origin (i0-1, j0-1, k0-2)
-                auto P = [&](int di, int dj, int dk) -> double {
-                    return sp[((li + 1 + di) * (TJ + 2) + (lj + 1 + dj)) * (KC + 4) + (kk + 2 + dk)];
-                };
-                // vn box: [TI+1][3][TJ+1][KC], origin (i0-1, colour 0, j0-1, k0)
-                auto VN = [&](int c, int di, int dj) -> double {
-                    return sv[(((li + 1 + di) * 3 + c) * (TJ + 1) + (lj + 1 + dj)) * KC + kk];
-                };
-                const double p0 = P(0, 0, 0);
+                const double *P = sp + kk;
+                const double *V = sv + kk;
+                const double p0 = P[0];
                 // the six incident edges in V->E slot order (connectivity.py:66); the
                 // origin is E->V slot 0 (connectivity.py:38-42)
-                const double f0 = edge_flux<OP>(p0, P(0, 1, 0), VN(0, 0, 0));
-                const double f1 = edge_flux<OP>(p0, P(1, 1, 0), VN(1, 0, 0));
-                const double f2 = edge_flux<OP>(p0, P(1, 0, 0), VN(2, 0, 0));
-                const double f3 = edge_flux<OP>(P(0, -1, 0), p0, VN(0, 0, -1));
-                const double f4 = edge_flux<OP>(P(-1, -1, 0), p0, VN(1, -1, -1));
-                const double f5 = edge_flux<OP>(P(-1, 0, 0), p0, VN(2, -1, 0));
+                const double f0 = edge_flux<OP>(p0, P[sPj], V[0]);
+                const double f1 = edge_flux<OP>(p0, P[sPi + sPj], V[sVc]);
+                const double f2 = edge_flux<OP>(p0, P[sPi], V[2 * sVc]);
+                const double f3 = edge_flux<OP>(P[-sPj], p0, V[-KC]);
+                const double f4 = edge_flux<OP>(P[-sPi - sPj], p0, V[-sVi + sVc - KC]);
+                const double f5 = edge_flux<OP>(P[-sPi], p0, V[-sVi + 2 * sVc]);
                 // interface fluxes fluz(k), fluz(k+1) (reference.py:38-60)
-                const double *W = sw + (li * TJ + lj) * (KC + 2) + kk;  // W[0] = wn(k)
-                double fz_lo = fluz_interior(W[0], P(0, 0, -1), p0);
-                double fz_hi = fluz_interior(W[1], p0, P(0, 0, 1));
-                if (k == 0) fz_lo = mul(a.pivbz, fz_hi);
-                if (k == a.K - 1) fz_hi = mul(a.pivbz, fz_lo);
+                const double *W = sw + kk;  // W[0] = wn(k)
+                double fz_lo = fluz_interior(W[0], P[-1], p0);
+                double fz_hi = fluz_interior(W[1], p0, P[1]);
+                if (chunk == 0 && k == 0) fz_lo = mul(a.pivbz, fz_hi);
+                if (chunk == last_chunk && k == a.K - 1) fz_hi = mul(a.pivbz, fz_lo);
                 // signed divergence (reference.py:63-79), canonical slot order from 0.0
                 double acc = 0.0;
                 acc = add(mul(sg0, f0), acc);
@@ -248,8 +273,22 @@ __global__ void __launch_bounds__(TI *TJ * 16)
                 const double div = dvd(acc, dual);
                 // explicit update (reference.py:82-90)
                 double slope = mul(a.dt, div);
-                slope = dvd(slope, sr[(li * TJ + lj) * KC + kk]);
-                store_img(a.pd_out, Fv, i, 0, j, k, sub(p0, slope), a.flags);
+                slope = dvd(slope, sr[kk]);
+                const double val = sub(p0, slope);
+                double *o = out + k;
+                o[0] = val;
+                if (d_row | d_col) {  // periodic halo images of boundary vertices
+                    if (d_row) o[d_row] = val;
+                    if (d_col) o[d_col] = val;
+                    if (d_row && d_col) o[d_row + d_col] = val;
+                }
+            }
+        }
+        if (++chunk == a.chunks) {
+            chunk = 0;
+            if (++tj == a.tiles_j) {
+                tj = 0;
+                ++ti;
             }
         }
         __syncthreads();  // every thread is done with this stage
@@ -314,7 +353,10 @@ static Variant *variants(int *count) {
         make_variant<4, 8, 16, 3>(),   // 2: 512 threads, 2 CTAs/SM
         make_variant<8, 8, 16, 3>(),   // 3: 1024 threads, 3 x 62.9 KB
         make_variant<2, 16, 32, 3>(),  // 4: 512 threads, 2 levels/thread
-        make_variant<4, 8, 16, 5>(),   // 5: 512 threads, 1 CTA/SM, 5 stages
+        make_variant<4, 8, 32, 3>(),   // 5: 512 threads, 2 levels/thread
+        make_variant<8, 8, 16, 2>(),   // 6: 1024 threads, 2 stages
+        make_variant<2, 32, 16, 3>(),  // 7: 1024 threads, long rows
+        make_variant<4, 16, 16, 2>(),  // 8: 1024 threads, 2 stages
     };
     *count = (int)(sizeof(v) / sizeof(v[0]));
     return v;
@@ -331,7 +373,7 @@ extern "C" int tsg_set_fused_variant(int variant) {
     variants(&n);
     if (variant < 0 || variant > n) return fail(TSG_EVALUE, "fused variant must be in [0, %d]", n);
     g_variant = variant == 0 ? 1 : variant;
-    return g_variant;
+    return TSG_OK;
 }
 
 extern "C" int tsg_fused_variant_info(int variant, int *ti, int *tj, int *kc, int *stages,
@@ -406,6 +448,7 @@ extern "C" int tsg_mpdata_step(tsg_grid *g, const double *pd, const double *vn, 
     a.tiles_j = (cols + v.tj - 1) / v.tj;
     a.chunks = (K + v.kc - 1) / v.kc;
     a.units = (int64_t)tiles_i * a.tiles_j * a.chunks;
+    if (a.units >= (1LL << 31)) return fail(TSG_EVALUE, "patch too large for one fused launch");
 
     void *fn = v.fn[flux_op];
     TSG_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
