@@ -33,8 +33,11 @@ def _core(rows, cols, colors, levels):
 
 
 def transport_inputs(rows: int, cols: int, levels: int, seed: int = 0, geometry: str = "uniform",
-                     preset: str = "gaussian-bump", rho: str = "one") -> dict:
-    """Flat [element, level] inputs of one transport step (canonical numbering)."""
+                     preset: str = "gaussian-bump", rho: str = "one", signs: bool = True) -> dict:
+    """Flat [element, level] inputs of one transport step (canonical numbering).
+
+    ``signs=False`` skips the device-built orientation signs (host-only use).
+    """
     from .connectivity import edge_signs_table
     from .topology import PatchSpec
 
@@ -72,12 +75,14 @@ def transport_inputs(rows: int, cols: int, levels: int, seed: int = 0, geometry:
     else:
         raise ValueError(f"unknown rho mode {rho!r}")
     nv = rows * cols
-    return {
+    out = {
         "pd": pd.reshape(nv, levels), "vn": vn.reshape(3 * nv, levels),
         "wn": wn.reshape(nv, levels + 1), "rho": rho_v.reshape(nv, levels),
         "dual": dual, "length": length, "area": area,
-        "signs": edge_signs_table(PatchSpec(rows, cols, levels)),
     }
+    if signs:
+        out["signs"] = edge_signs_table(PatchSpec(rows, cols, levels))
+    return out
 
 
 def mpdata_algorithmic_bytes(rows: int, cols: int, levels: int) -> int:
