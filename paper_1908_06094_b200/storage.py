@@ -242,6 +242,8 @@ def sync(field: Field, to_space: str) -> None:
     if field.dirty[src]:
         grid = device_grid(field.spec)
         lay = field.linear.layout6()
+        if not field.has_levels:
+            lay[4] = 0  # the device inner axis runs along `extra` (or is a scalar)
         lay_p = lay.ctypes.data_as(_lib.ctypes.POINTER(_lib.ctypes.c_int64))
         if to_space == "mirror":
             staging = torch.from_numpy(field.buffer("primary")).to(grid.device)

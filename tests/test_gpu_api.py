@@ -1,0 +1,335 @@
+"""GPU tests of the drop-in API (Fields, runners, reductions, layouts) against the oracle /
+the reference's golden vectors.  Mirrors the reference's own tests:
+C3 (fused == naive), C4 (== flat oracle), C6 (renumbering), C8 (conservation), plus edge
+cases (2 levels, odd level counts, 2x2 patches, ragged tiles, NaN / signed zero) and
+size-independent properties at O1280-class scale.  Floating-point checks are bitwise
+(np.array_equal), stricter than the north-star 1e-12 relative tolerance."""
+
+import numpy as np
+import pytest
+
+from oracle import tsg_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+T = pytest.importorskip("paper_1908_06094_b200")
+L = T.LocationType
+
+
+def _fill(field, rng, lo, hi):
+    spec = field.spec
+    h = spec.halo
+    arr = field.array("primary", "rw")
+    shape = arr[h:h + spec.rows, :, h:h + spec.cols, :, :].shape
+    arr[h:h + spec.rows, :, h:h + spec.cols, :, :] = lo + (hi - lo) * rng.random(shape)
+    T.halo_update(field)
+
+
+def _case(spec, seed, geometry="random", layout=None):
+    """tests/test_mpdata.py:_setup of the reference, through our Field API."""
+    geo = T.build_geometry(spec, geometry, seed=seed, layout=layout)
+    state = T.build_state(spec, layout=layout)
+    rng = np.random.default_rng(seed)
+    T.init_preset(state.pd_in, "random", seed=seed)
+    _fill(state.vn, rng, -0.5, 0.5)
+    _fill(state.wn, rng, -0.5, 0.5)
+    _fill(state.rho, rng, 0.5, 1.5)
+    return geo, state
+
+
+def _oracle(spec, geo, state, params, op="upwind"):
+    r, c = spec.rows, spec.cols
+    return O.transport_step(O.neighbor_table(r, c, "edges", "vertices"),
+                            O.neighbor_table(r, c, "vertices", "edges"), O.edge_signs(r, c),
+                            T.field_to_flat(geo.dual_volumes)[:, 0], T.field_to_flat(state.pd_in),
+                            T.field_to_flat(state.vn), T.field_to_flat(state.wn),
+                            T.field_to_flat(state.rho), params.dt, params.pivbz, op)
+
+
+@pytest.mark.parametrize("shape,seed", [((4, 4, 3), 0), ((5, 3, 4), 1), ((8, 8, 8), 2), ((2, 2, 2), 3),
+                                        ((7, 19, 33), 4), ((3, 41, 2), 5)])
+def test_field_api_naive_and_fused_match_oracle(cuda_ok, shape, seed):
+    spec = T.PatchSpec(*shape)
+    params = T.MpdataParams(dt=0.2, pivbz=0.7)
+    geo, state = _case(spec, seed)
+    want = _oracle(spec, geo, state, params)
+    comp = T.build_mpdata(spec, state, geo, params)
+    stats = T.run_naive(comp)
+    assert stats.total_updates == spec.rows * spec.cols * (6 * spec.levels + 1)
+    assert np.array_equal(T.field_to_flat(state.flux), want["flux"])
+    assert np.array_equal(T.field_to_flat(state.fluz), want["fluz"])
+    assert np.array_equal(T.field_to_flat(state.divvd), want["div"])
+    assert np.array_equal(T.field_to_flat(state.pd_out), want["pd_out"])
+    T.run_fused(comp, T.TileSpec(2, 2))
+    assert np.array_equal(T.field_to_flat(state.pd_out), want["pd_out"])
+    # halo of the output is a periodic image, like after the reference's halo_update
+    arr = state.pd_out.array()
+    assert np.array_equal(arr[0], arr[spec.rows]) and np.array_equal(arr[:, :, -1], arr[:, :, 1])
+
+
+def test_level_inner_layout_and_wide_halo(cuda_ok):
+    spec = T.PatchSpec(6, 5, 4, halo=2)
+    lay = T.LayoutSpec(("extra", "row", "color", "column", "level"), 8)
+    params = T.MpdataParams(dt=0.15, pivbz=0.3)
+    geo, state = _case(spec, 12, layout=lay)
+    want = _oracle(spec, geo, state, params)
+    T.run_fused(T.build_mpdata(spec, state, geo, params))
+    assert np.array_equal(T.field_to_flat(state.pd_out), want["pd_out"])
+    arr = state.pd_out.array()  # halo width 2 filled with periodic images
+    assert np.array_equal(arr[:2], arr[6:8]) and np.array_equal(arr[:, :, 7:9], arr[:, :, 2:4])
+
+
+def test_centred_operator_and_validation(cuda_ok):
+    spec = T.PatchSpec(5, 4, 3)
+    geo, state = _case(spec, 3)
+    params = T.MpdataParams()
+    want = _oracle(spec, geo, state, params, "centred")
+    comp = T.build_mpdata(spec, state, geo, params, flux_op="centred")
+    T.run_fused(comp)
+    assert np.array_equal(T.field_to_flat(state.pd_out), want["pd_out"])
+    T.run_naive(comp)
+    assert np.array_equal(T.field_to_flat(state.flux), want["flux"])
+    with pytest.raises(ValueError, match="operator"):
+        T.build_mpdata(spec, state, geo, params, flux_op="sideways")
+    with pytest.raises(ValueError, match="levels"):
+        s1 = T.PatchSpec(4, 4, 1)
+        g1, st1 = _case(s1, 0)
+        T.build_mpdata(s1, st1, g1, params)
+    state.rho.array("primary", "rw")[:] = 0.0
+    with pytest.raises(ValueError, match="rho"):
+        T.build_mpdata(spec, state, geo, params)
+
+
+def test_fluz_boundaries_copy_at_unit_pivbz(cuda_ok):
+    spec = T.PatchSpec(4, 4, 4)
+    geo, state = _case(spec, 6)
+    T.run_naive(T.build_mpdata(spec, state, geo, T.MpdataParams(pivbz=1.0)))
+    fluz = T.field_to_flat(state.fluz)
+    assert np.array_equal(fluz[:, -1], fluz[:, -2]) and np.array_equal(fluz[:, 0], fluz[:, 1])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_closed_system_conserves_mass(cuda_ok, seed):
+    """Acceptance C8: pivbz = 0, rho = 1 -> mass drift <= 1e-12 (device reduction)."""
+    spec = T.PatchSpec(*[(6, 6, 4), (8, 4, 5), (5, 7, 3), (4, 4, 2), (33, 17, 9), (64, 64, 20)][seed])
+    geo, state = _case(spec, seed)
+    T.init_preset(state.rho, "uniform")
+    comp = T.build_mpdata(spec, state, geo, T.MpdataParams(dt=0.05, pivbz=0.0))
+    m0 = T.total_mass(state, geo, "pd_in")
+    T.run_gpu(comp, download=False)
+    m1 = T.total_mass(state, geo, "pd_out")
+    assert abs(m1 - m0) <= 1e-12 * abs(m0)
+    host = float(np.sum(T.field_to_flat(state.pd_in) * T.field_to_flat(geo.dual_volumes)))
+    assert abs(m0 - host) <= 1e-13 * abs(host)
+
+
+def test_relabelled_flat_paths_are_invariant(cuda_ok, golden):
+    """Indirect path under HN/UN numberings, and the structured stepper fed renumbered data."""
+    spec = T.PatchSpec(4, 4, 3)
+    inp = O.transport_inputs(4, 4, 3, 5, "random", "random", "random")
+    base = O.step_inputs(4, 4, inp, 0.1, 0.4)
+    pv = T.make_permutation(T.Numbering.HN, spec, L.VERTICES)
+    pe = T.make_permutation(T.Numbering.UN, spec, L.EDGES)
+    e2v = T.build_neighbor_table(spec, L.EDGES, L.VERTICES, pe, pv).ids
+    v2e = T.build_neighbor_table(spec, L.VERTICES, L.EDGES, pv, pe).ids
+    assert np.array_equal(e2v, golden["tblp_relabel_4x4_edges_vertices"])
+    out = T.transport_step(e2v, v2e, inp["signs"][pv.inverse], inp["dual"][pv.inverse],
+                           inp["pd"][pv.inverse], inp["vn"][pe.inverse], inp["wn"][pv.inverse],
+                           inp["rho"][pv.inverse], 0.1, 0.4)
+    assert np.array_equal(out["pd_out"][pv.forward], base["pd_out"])
+    assert np.array_equal(out["flux"][pe.forward], base["flux"])
+    st = T.StructuredStepper(spec, perm_v=pv, perm_e=pe)
+    st.set_geometry(inp["signs"][pv.inverse], inp["dual"][pv.inverse])
+    got = st(inp["pd"][pv.inverse], inp["vn"][pe.inverse], inp["wn"][pv.inverse],
+             inp["rho"][pv.inverse], 0.1, 0.4)
+    assert np.array_equal(got[pv.forward], base["pd_out"])
+
+
+def test_table1_kernels_direct_and_indirect(cuda_ok, golden):
+    """Acceptance C6: direct structured and SN/UN/HN indirect sweeps agree bitwise."""
+    for r, c, lev in ((16, 8, 2), (5, 7, 3)):
+        key = f"k_{r}x{c}x{lev}"
+        spec = T.PatchSpec(r, c, lev)
+        fields = T.make_kernel_fields(spec)
+        T.flat_to_field(golden[f"{key}_a"], fields["a"])
+        T.flat_to_field(golden[f"{key}_fac"], fields["fac"])
+        for scaled, tag in ((False, "k1"), (True, "k2")):
+            T.run_naive(T.build_kernel(spec, fields, scaled))
+            assert np.array_equal(T.field_to_flat(fields["b"]), golden[f"{key}_{tag}"]), tag
+            for num in T.Numbering:
+                perm = T.make_permutation(num, spec, L.CELLS)
+                table = T.build_neighbor_table(spec, L.CELLS, L.CELLS, perm, perm)
+                a = T.field_to_flat(fields["a"], perm)
+                got = (T.run_neighbor_sum_scaled(table, a, T.field_to_flat(fields["fac"], perm))
+                       if scaled else T.run_neighbor_sum(table, a))
+                assert np.array_equal(T.unpermute(got, perm), golden[f"{key}_{tag}"]), (tag, num)
+
+
+def test_nine_relation_reduce(cuda_ok, golden):
+    spec = T.PatchSpec(6, 5, 3)
+    for (f, t) in T.OFFSET_TABLES:
+        src = T.make_storage(spec, t, "a")
+        dst = T.make_storage(spec, f, "b")
+        T.flat_to_field(golden[f"red_{f.value}_{t.value}_a"], src)
+        T.run_gpu(T.build_reduce(spec, f, t, src, dst))
+        assert np.array_equal(T.field_to_flat(dst), golden[f"red_{f.value}_{t.value}_b"]), (f, t)
+
+
+def test_cell_divergence_and_weights(cuda_ok, golden):
+    spec = T.PatchSpec(5, 5, 3)
+    geo, state = _case(spec, 7)
+    assert np.array_equal(T.field_to_flat(state.vn), golden["cdiv_vn"])
+    w = geo.weights.core()[:, :, :, 0, :].reshape(-1, 3)
+    assert np.array_equal(w, golden["cdiv_weights"])
+    for weighted in (False, True):
+        out = T.make_storage(spec, L.CELLS, "div_out")
+        T.run_naive(T.build_divergence(spec, state, geo, weighted=weighted, out=out))
+        assert np.array_equal(T.field_to_flat(out), golden[f"cdiv_{int(weighted)}"])
+
+
+def test_pack_unpack_roundtrip_every_numbering(cuda_ok):
+    import torch
+
+    spec = T.PatchSpec(9, 7, 5)
+    for loc in L:
+        f = T.make_storage(spec, loc, "x")
+        n = T.element_count(spec, loc)
+        vals = torch.rand((n, 5), dtype=torch.float64, device="cuda")
+        for num in T.Numbering:
+            if num is T.Numbering.HN and loc is L.EDGES:
+                continue
+            perm = T.make_permutation(num, spec, loc)
+            T.flat_to_field(vals, f, perm)
+            assert np.array_equal(T.field_to_flat(f, perm), vals.cpu().numpy()), (loc, num)
+            # halo images written by the pack kernel
+            dev = f.device().cpu().numpy()
+            assert np.array_equal(dev[0, :, 1:-1], dev[spec.rows, :, 1:-1])
+            assert np.array_equal(dev[:, :, 0], dev[:, :, spec.cols])
+
+
+def test_device_halo_update_matches_host(cuda_ok):
+    spec = T.PatchSpec(5, 6, 4)
+    f = T.make_storage(spec, L.CELLS, "c")
+    _fill(f, np.random.default_rng(1), 0, 1)
+    dev = f.ensure_device()
+    r, c = spec.rows, spec.cols
+    dev[0].zero_()
+    dev[:, :, -1].zero_()
+    dev[r + 1].fill_(7.0)
+    T.halo_update(f, "mirror")
+    d = dev.cpu().numpy()
+    assert np.array_equal(d[0], d[r]) and np.array_equal(d[r + 1], d[1])
+    assert np.array_equal(d[:, :, 0], d[:, :, c]) and np.array_equal(d[:, :, c + 1], d[:, :, 1])
+    T.sync(f, "primary")
+    assert np.array_equal(f.array()[0], f.array()[r])
+
+
+@pytest.mark.parametrize("shape", [(6, 5, 2), (6, 5, 137), (2, 2, 3), (11, 3, 17), (4, 70, 81)])
+def test_edge_shapes_fused_unfused_indirect(cuda_ok, shape):
+    from tests.gpu_helpers import fused_step, oracle_tables, unfused_step
+
+    r, c, lev = shape
+    inp = O.transport_inputs(r, c, lev, 9, "random", "random", "random")
+    want = O.step_inputs(r, c, inp, 0.2, 0.8)
+    assert np.array_equal(fused_step(r, c, lev, inp, 0.2, 0.8), want["pd_out"])
+    got = unfused_step(r, c, lev, inp, 0.2, 0.8)
+    for k in want:
+        assert np.array_equal(got[k], want[k]), k
+    e2v, v2e = oracle_tables(r, c)
+    out = T.transport_step(e2v, v2e, inp["signs"], inp["dual"], inp["pd"], inp["vn"], inp["wn"],
+                           inp["rho"], 0.2, 0.8)
+    for k in want:
+        assert np.array_equal(out[k], want[k]), k
+
+
+def test_nan_and_signed_zero_semantics(cuda_ok):
+    """numpy.maximum/minimum semantics: NaN propagates, -0.0 velocities give +0.0 terms."""
+    from tests.gpu_helpers import fused_step, unfused_step
+
+    r, c, lev = 6, 7, 5
+    inp = O.transport_inputs(r, c, lev, 2, "random", "random", "random")
+    inp["vn"][3, 2] = np.nan
+    inp["vn"][10, 1] = -0.0
+    inp["vn"][11, :] = 0.0
+    inp["wn"][4, 2] = np.nan
+    inp["wn"][5, 3] = -0.0
+    inp["pd"][7, :] = -0.0
+    want = O.step_inputs(r, c, inp, 0.2, 0.8)
+    got = fused_step(r, c, lev, inp, 0.2, 0.8)
+    assert np.array_equal(np.isnan(got), np.isnan(want["pd_out"]))
+    assert np.array_equal(got, want["pd_out"], equal_nan=True)
+    assert np.array_equal(np.signbit(got), np.signbit(want["pd_out"]))
+    un = unfused_step(r, c, lev, inp, 0.2, 0.8)
+    for k in want:
+        assert np.array_equal(un[k], want[k], equal_nan=True), k
+        assert np.array_equal(np.signbit(un[k]), np.signbit(want[k])), k
+
+
+def test_every_fused_variant_is_bitwise_identical(cuda_ok):
+    from paper_1908_06094_b200 import _lib
+    from tests.gpu_helpers import fused_step
+
+    r, c, lev = 37, 45, 50
+    inp = O.transport_inputs(r, c, lev, 4, "random", "random", "random")
+    want = O.step_inputs(r, c, inp, 0.2, 0.8)["pd_out"]
+    try:
+        for v in range(1, 9):
+            _lib.call("tsg_set_fused_variant", v)
+            assert np.array_equal(fused_step(r, c, lev, inp, 0.2, 0.8), want), v
+    finally:
+        _lib.call("tsg_set_fused_variant", 0)
+
+
+def test_o1280_class_properties(cuda_ok):
+    """At a quarter of the O1280 patch (640 x 2576 x 137, 7.4 GB of state): the fused kernel
+    equals the independent four-kernel path bitwise, and a closed system conserves mass."""
+    import torch
+
+    from paper_1908_06094_b200 import _lib
+    from paper_1908_06094_b200.device import DeviceGrid
+
+    rows, cols, K = 640, 2576, 137
+    g = DeviceGrid(rows, cols, K)
+    s = _lib.stream_handle()
+    fields = {}
+    for seed, (name, loc, inner, lo, hi) in enumerate((("pd", 0, K, 0.0, 1.0), ("vn", 2, K, -0.5, 0.5),
+                                                       ("wn", 0, K + 1, -0.5, 0.5), ("rho", 0, K, 1.0, 1.0))):
+        fields[name] = g.empty(loc, inner)
+        _lib.call("tsg_fill_hash", g.handle, loc, inner, seed + 1, lo, hi,
+                  _lib.ptr(fields[name]), s)
+    signs = g.empty(0, 6)
+    flat = torch.empty((rows * cols, 6), dtype=torch.float64, device="cuda")
+    _lib.call("tsg_edge_signs", rows, cols, _lib.ptr(flat), s)
+    _lib.call("tsg_pack", g.handle, 0, 6, _lib.ptr(flat), None, _lib.ptr(signs), s)
+    del flat
+    dual = g.empty(0, 1)
+    _lib.call("tsg_fill_hash", g.handle, 0, 1, 99, 0.5, 1.5, _lib.ptr(dual), s)
+    a, b = g.empty(0, K), g.empty(0, K)
+    ins = [_lib.ptr(fields[n]) for n in ("pd", "vn", "wn", "rho")] + [_lib.ptr(signs), _lib.ptr(dual)]
+    _lib.call("tsg_mpdata_step", g.handle, *ins, _lib.ptr(a), 0.05, 0.0, 0, s)
+    flux, fluz, div = g.empty(2, K), g.empty(0, K + 1), g.empty(0, K)
+    _lib.call("tsg_mpdata_step_unfused", g.handle, *ins, _lib.ptr(flux), _lib.ptr(fluz), _lib.ptr(div),
+              _lib.ptr(b), 0.05, 0.0, 0, s)
+    assert torch.equal(a, b)
+    work = torch.empty(1026, dtype=torch.float64, device="cuda")
+    _lib.call("tsg_total_mass", g.handle, _lib.ptr(fields["pd"]), _lib.ptr(dual), _lib.ptr(work[:1024]),
+              _lib.ptr(work[1024:1025]), s)
+    _lib.call("tsg_total_mass", g.handle, _lib.ptr(a), _lib.ptr(dual), _lib.ptr(work[:1024]),
+              _lib.ptr(work[1025:]), s)
+    m0, m1 = work[1024].item(), work[1025].item()
+    assert abs(m1 - m0) <= 1e-12 * abs(m0)
+
+
+def test_fill_hash_is_decomposition_invariant(cuda_ok):
+    from paper_1908_06094_b200 import _lib
+    from paper_1908_06094_b200.device import PERIODIC_COLS, DeviceGrid
+
+    s = _lib.stream_handle()
+    full = DeviceGrid(12, 9, 5)
+    f = full.empty(2, 5)
+    _lib.call("tsg_fill_hash", full.handle, 2, 5, 7, -1.0, 1.0, _lib.ptr(f), s)
+    for r0, nr in ((0, 4), (4, 5), (9, 3)):
+        strip = DeviceGrid(nr, 9, 5, flags=PERIODIC_COLS, row0=r0, global_rows=12)
+        t = strip.empty(2, 5)
+        _lib.call("tsg_fill_hash", strip.handle, 2, 5, 7, -1.0, 1.0, _lib.ptr(t), s)
+        assert np.array_equal(t[1:nr + 1].cpu().numpy(), f[r0 + 1:r0 + nr + 1].cpu().numpy())
