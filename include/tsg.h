@@ -105,6 +105,12 @@ int tsg_unpack_strided(const tsg_grid *g, int loc, int inner, const double *fiel
 int tsg_mpdata_step(tsg_grid *g, const double *pd, const double *vn, const double *wn,
                     const double *rho, const double *signs, const double *dual, double *pd_out,
                     double dt, double pivbz, int flux_op, tsg_stream s);
+/* Same step restricted to logical rows [row_lo, row_hi) -- lets a row strip compute its
+ * interior while its halo rows are still in flight, then its two boundary rows. */
+int tsg_mpdata_step_rows(tsg_grid *g, const double *pd, const double *vn, const double *wn,
+                         const double *rho, const double *signs, const double *dual,
+                         double *pd_out, double dt, double pivbz, int flux_op, int row_lo,
+                         int row_hi, tsg_stream s);
 /* Four-kernel step materialising flux (edges), fluz (vertices, levels+1) and divvd
  * (vertices) like run_naive (executors.py:213-245), halos refreshed after each stage. */
 int tsg_mpdata_step_unfused(const tsg_grid *g, const double *pd, const double *vn,

@@ -32,6 +32,8 @@ SIGNATURES = {
     "tsg_pack_strided": (_c_int, [_p, _c_int, _c_int, _p, ctypes.POINTER(_c_i64), _c_int, _p, _p]),
     "tsg_unpack_strided": (_c_int, [_p, _c_int, _c_int, _p, ctypes.POINTER(_c_i64), _c_int, _p, _p]),
     "tsg_mpdata_step": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _c_dbl, _c_dbl, _c_int, _p]),
+    "tsg_mpdata_step_rows": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _c_dbl, _c_dbl, _c_int, _c_int,
+                                      _c_int, _p]),
     "tsg_mpdata_step_unfused": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _c_dbl,
                                          _c_dbl, _c_int, _p]),
     "tsg_transport_indirect": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _c_i64, _c_i64, _c_int,

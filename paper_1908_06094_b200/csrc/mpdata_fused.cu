@@ -118,6 +118,7 @@ struct FusedArgs {
     const double *dual;   // vertex field, inner 1
     double *pd_out;       // vertex field, inner K
     int rows, cols, K;
+    int row_lo, row_hi;  // rows computed by this launch: [row_lo, row_hi)
     int flags;
     double dt, pivbz;
     int tiles_j, chunks;
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(TI *TJ * 16)
     int p_chunk = u_begin % a.chunks, p_tile = u_begin / a.chunks;
     int p_ti = p_tile / a.tiles_j, p_tj = p_tile % a.tiles_j;
     auto issue_next = [&](int stage) {
-        const int i0 = p_ti * TI, j0 = p_tj * TJ, k0 = p_chunk * KC;
+        const int i0 = a.row_lo + p_ti * TI, j0 = p_tj * TJ, k0 = p_chunk * KC;
         unsigned char *base = smem + stage * C::kStageBytes;
         uint64_t *bar = &bars[stage];
         mbar_expect_tx(bar, C::kTxBytes);
@@ -209,8 +210,8 @@ __global__ void __launch_bounds__(TI *TJ * 16)
             issue_next((n + STAGES - 1) % STAGES);
         }
         if (n == 0 || chunk == 0) {
-            const int i = ti * TI + li, j = tj * TJ + lj;
-            vvalid = i < a.rows && j < a.cols;
+            const int i = a.row_lo + ti * TI + li, j = tj * TJ + lj;
+            vvalid = i < a.row_hi && j < a.cols;
             if (vvalid) {
                 const int64_t cell = (int64_t)(i + 1) * (a.cols + 2) + (j + 1);
                 const double *S = a.signs + cell * 6;
@@ -396,6 +397,18 @@ extern "C" int tsg_mpdata_step(tsg_grid *g, const double *pd, const double *vn, 
                                const double *rho, const double *signs, const double *dual,
                                double *pd_out, double dt, double pivbz, int flux_op, tsg_stream s) {
     if (!g) return fail(TSG_EVALUE, "grid is NULL");
+    return tsg_mpdata_step_rows(g, pd, vn, wn, rho, signs, dual, pd_out, dt, pivbz, flux_op, 0,
+                                g->rows, s);
+}
+
+extern "C" int tsg_mpdata_step_rows(tsg_grid *g, const double *pd, const double *vn,
+                                    const double *wn, const double *rho, const double *signs,
+                                    const double *dual, double *pd_out, double dt, double pivbz,
+                                    int flux_op, int row_lo, int row_hi, tsg_stream s) {
+    if (!g) return fail(TSG_EVALUE, "grid is NULL");
+    if (row_lo < 0 || row_hi > g->rows || row_lo > row_hi)
+        return fail(TSG_EVALUE, "row range [%d, %d) outside [0, %d)", row_lo, row_hi, g->rows);
+    if (row_lo == row_hi) return TSG_OK;
     const int K = g->levels;
     if (K < 2) return fail(TSG_EVALUE, "the transport step needs at least 2 levels, got %d", K);
     if (flux_op != TSG_UPWIND && flux_op != TSG_CENTRED)
@@ -440,11 +453,13 @@ extern "C" int tsg_mpdata_step(tsg_grid *g, const double *pd, const double *vn, 
     a.pd_out = pd_out;
     a.rows = rows;
     a.cols = cols;
+    a.row_lo = row_lo;
+    a.row_hi = row_hi;
     a.K = K;
     a.flags = g->flags;
     a.dt = dt;
     a.pivbz = pivbz;
-    const int tiles_i = (rows + v.ti - 1) / v.ti;
+    const int tiles_i = (row_hi - row_lo + v.ti - 1) / v.ti;
     a.tiles_j = (cols + v.tj - 1) / v.tj;
     a.chunks = (K + v.kc - 1) / v.kc;
     a.units = (int64_t)tiles_i * a.tiles_j * a.chunks;
