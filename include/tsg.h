@@ -105,7 +105,10 @@ int tsg_unpack_strided(const tsg_grid *g, int loc, int inner, const double *fiel
 int tsg_mpdata_step(tsg_grid *g, const double *pd, const double *vn, const double *wn,
                     const double *rho, const double *signs, const double *dual, double *pd_out,
                     double dt, double pivbz, int flux_op, tsg_stream s);
-/* Same step restricted to logical rows [row_lo, row_hi) -- lets a row strip compute its
+/* flux_op = 99 runs the fused kernel's data-movement probe (TMA pipeline and stores
+ * only, no arithmetic) and flux_op = 98 its compute probe (arithmetic on shared memory
+ * that is never loaded) -- benchmarking aids for the memory and compute ceilings.
+ * Same step restricted to logical rows [row_lo, row_hi) -- lets a row strip compute its
  * interior while its halo rows are still in flight, then its two boundary rows. */
 int tsg_mpdata_step_rows(tsg_grid *g, const double *pd, const double *vn, const double *wn,
                          const double *rho, const double *signs, const double *dual,

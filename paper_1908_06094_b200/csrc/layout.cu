@@ -18,36 +18,52 @@ static inline int grid_for(int64_t work, int threads, int num_sms) {
 
 // -- pack / unpack: the "Atlas -> structured" reorder (kernels.py:107-134) ------------
 
-__global__ void pack_kernel(FieldIx F, int inner, const double *__restrict__ flat,
+__global__ void pack_kernel(FieldIx F, int inner, PointDec D, const double *__restrict__ flat,
                             const int64_t *__restrict__ forward, double *__restrict__ f,
                             int flags) {
-    const int64_t n = (int64_t)F.rows * F.colors * F.cols * inner;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t id = t / inner;
-        int k = (int)(t - id * inner);
-        int j = (int)(id % F.cols);
-        int64_t rest = id / F.cols;
-        int c = (int)(rest % F.colors);
-        int i = (int)(rest / F.colors);
+    TSG_POINTS(t, D) {
+        const Pt p = decompose(t, D);
+        const int i = p.i, c = p.c, j = p.j, k = p.k;
+        const int64_t id = p.e;
         int64_t rank = forward ? forward[id] : id;
         store_img(f, F, i, c, j, k, flat[rank * inner + k], flags);
     }
 }
 
-__global__ void unpack_kernel(FieldIx F, int inner, const double *__restrict__ f,
+__global__ void unpack_kernel(FieldIx F, int inner, PointDec D, const double *__restrict__ f,
                               const int64_t *__restrict__ forward, double *__restrict__ flat) {
-    const int64_t n = (int64_t)F.rows * F.colors * F.cols * inner;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t id = t / inner;
-        int k = (int)(t - id * inner);
-        int j = (int)(id % F.cols);
-        int64_t rest = id / F.cols;
-        int c = (int)(rest % F.colors);
-        int i = (int)(rest / F.colors);
+    TSG_POINTS(t, D) {
+        const Pt p = decompose(t, D);
+        const int i = p.i, c = p.c, j = p.j, k = p.k;
+        const int64_t id = p.e;
         int64_t rank = forward ? forward[id] : id;
         flat[rank * inner + k] = f[F.at(i, c, j) + k];
+    }
+}
+
+// element-line variants (one warp per element, lanes along the level run) for long runs
+__global__ void __launch_bounds__(256, 6) pack_lines_kernel(FieldIx F, int inner,
+                                                         const double *__restrict__ flat,
+                                                         const int64_t *__restrict__ forward,
+                                                         double *__restrict__ f, int flags) {
+    TSG_LINES(F, i, c, j) {
+        const int64_t id = ((int64_t)i * F.colors + c) * F.cols + j;
+        const double *src = flat + (forward ? __ldg(forward + id) : id) * inner;
+        double *o = f + F.at(i, c, j);
+        const Img m = images(F, i, j, flags);
+        for (int k = threadIdx.x; k < inner; k += 32) put(o, m, k, src[k]);
+    }
+}
+
+__global__ void __launch_bounds__(256, 6) unpack_lines_kernel(FieldIx F, int inner,
+                                                           const double *__restrict__ f,
+                                                           const int64_t *__restrict__ forward,
+                                                           double *__restrict__ flat) {
+    TSG_LINES(F, i, c, j) {
+        const int64_t id = ((int64_t)i * F.colors + c) * F.cols + j;
+        double *dst = flat + (forward ? __ldg(forward + id) : id) * inner;
+        const double *src = f + F.at(i, c, j);
+        for (int k = threadIdx.x; k < inner; k += 32) dst[k] = src[k];
     }
 }
 
@@ -97,17 +113,12 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
     return x;
 }
 
-__global__ void fill_hash_kernel(FieldIx F, int inner, int row0, uint64_t seed, double lo,
-                                 double hi, double *__restrict__ f, int flags) {
-    const int64_t n = (int64_t)F.rows * F.colors * F.cols * inner;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t id = t / inner;
-        int k = (int)(t - id * inner);
-        int j = (int)(id % F.cols);
-        int64_t rest = id / F.cols;
-        int c = (int)(rest % F.colors);
-        int i = (int)(rest / F.colors);
+__global__ void fill_hash_kernel(FieldIx F, int inner, PointDec D, int row0, uint64_t seed,
+                                 double lo, double hi, double *__restrict__ f, int flags) {
+    TSG_POINTS(t, D) {
+        const Pt p = decompose(t, D);
+        const int i = p.i, c = p.c, j = p.j, k = p.k;
+        const int64_t id = p.e;
         // global canonical id of the element: decomposition-invariant
         uint64_t gid = ((uint64_t)(i + row0) * F.colors + c) * F.cols + j;
         uint64_t h = mix64(seed * 0x9e3779b97f4a7c15ULL + mix64(gid * 4099ULL + (uint64_t)k));
@@ -385,9 +396,14 @@ extern "C" int tsg_pack(const tsg_grid *g, int loc, int inner, const double *fla
     if (!valid_loc(loc) || inner < 1) return fail(TSG_EVALUE, "tsg_pack: bad location/inner");
     if (!flat || !field) return fail(TSG_EVALUE, "tsg_pack: NULL array");
     FieldIx F(g->rows, g->cols, colors_of(loc), inner);
-    int64_t n = (int64_t)g->rows * F.colors * g->cols * inner;
-    pack_kernel<<<grid_for(n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(F, inner, flat, forward,
-                                                                           field, g->flags);
+    if (!PointDec::fits(g->rows, g->cols, F.colors, inner)) return fail(TSG_EVALUE, "field too large");
+    PointDec D(g->rows, g->cols, F.colors, inner);
+    if (inner >= 16)
+        pack_lines_kernel<<<line_grid(g->cols, (int64_t)g->rows * F.colors, g->num_sms), line_block(), 0,
+                            (cudaStream_t)s>>>(F, inner, flat, forward, field, g->flags);
+    else
+        pack_kernel<<<grid_for(D.n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(F, inner, D, flat,
+                                                                                 forward, field, g->flags);
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }
@@ -398,9 +414,14 @@ extern "C" int tsg_unpack(const tsg_grid *g, int loc, int inner, const double *f
     if (!valid_loc(loc) || inner < 1) return fail(TSG_EVALUE, "tsg_unpack: bad location/inner");
     if (!flat || !field) return fail(TSG_EVALUE, "tsg_unpack: NULL array");
     FieldIx F(g->rows, g->cols, colors_of(loc), inner);
-    int64_t n = (int64_t)g->rows * F.colors * g->cols * inner;
-    unpack_kernel<<<grid_for(n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(F, inner, field,
-                                                                             forward, flat);
+    if (!PointDec::fits(g->rows, g->cols, F.colors, inner)) return fail(TSG_EVALUE, "field too large");
+    PointDec D(g->rows, g->cols, F.colors, inner);
+    if (inner >= 16)
+        unpack_lines_kernel<<<line_grid(g->cols, (int64_t)g->rows * F.colors, g->num_sms), line_block(), 0,
+                              (cudaStream_t)s>>>(F, inner, field, forward, flat);
+    else
+        unpack_kernel<<<grid_for(D.n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(F, inner, D, field,
+                                                                                   forward, flat);
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }
@@ -424,9 +445,10 @@ extern "C" int tsg_fill_hash(const tsg_grid *g, int loc, int inner, uint64_t see
     if (!valid_loc(loc) || inner < 1) return fail(TSG_EVALUE, "tsg_fill_hash: bad location/inner");
     if (!field) return fail(TSG_EVALUE, "tsg_fill_hash: NULL field");
     FieldIx F(g->rows, g->cols, colors_of(loc), inner);
-    int64_t n = (int64_t)g->rows * F.colors * g->cols * inner;
-    fill_hash_kernel<<<grid_for(n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(
-        F, inner, g->row0, seed, lo, hi, field, g->flags);
+    if (!PointDec::fits(g->rows, g->cols, F.colors, inner)) return fail(TSG_EVALUE, "field too large");
+    PointDec D(g->rows, g->cols, F.colors, inner);
+    fill_hash_kernel<<<grid_for(D.n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(
+        F, inner, D, g->row0, seed, lo, hi, field, g->flags);
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }

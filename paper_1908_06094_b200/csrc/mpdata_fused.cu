@@ -92,10 +92,10 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
 
 // ---- tile geometry --------------------------------------------------------------------
 
-template <int TI, int TJ, int KC, int STAGES>
+template <int TI, int TJ, int KC, int STAGES, int LV>
 struct FusedCfg {
-    static constexpr int kThreads = TI * TJ * 16;
-    static constexpr int kLevelsPerThread = KC / 16;
+    static constexpr int kThreads = TI * TJ * LV;                  // LV lanes per vertex
+    static constexpr int kLevelsPerThread = (KC + LV - 1) / LV;  // last pass may be partial
     static constexpr int kPdBytes = (TI + 2) * (TJ + 2) * (KC + 4) * 8;
     static constexpr int kVnBytes = (TI + 1) * 3 * (TJ + 1) * KC * 8;
     static constexpr int kWnBytes = TI * TJ * (KC + 2) * 8;
@@ -109,9 +109,15 @@ struct FusedCfg {
     static constexpr uint32_t kTxBytes = kPdBytes + kVnBytes + kWnBytes + kRhoBytes;
     static constexpr int kSmemBytes = STAGES * kStageBytes + 128;  // + barriers
     static_assert(KC % 16 == 0, "KC must be a multiple of 16");
+    static_assert(LV == 16 || LV == 32, "a half-warp or a warp per vertex");
     static_assert(((KC + 2) * 8) % 16 == 0 && (KC * 8) % 16 == 0, "TMA inner box must be 16B multiple");
     static_assert(TI + 2 <= 256 && TJ + 2 <= 256 && KC + 4 <= 256, "TMA box <= 256");
 };
+
+// flux_op value of the data-movement probe (benchmarking the TMA pipeline alone)
+constexpr int kProbeOp = 99;
+// flux_op value of the compute probe (arithmetic on unloaded shared memory, no TMA)
+constexpr int kComputeProbe = 98;
 
 struct FusedArgs {
     const double *signs;  // vertex field, inner 6
@@ -125,19 +131,19 @@ struct FusedArgs {
     int64_t units;
 };
 
-template <int TI, int TJ, int KC, int STAGES, int OP>
-__global__ void __launch_bounds__(TI *TJ * 16)
+template <int TI, int TJ, int KC, int STAGES, int LV, int OP>
+__global__ void __launch_bounds__(TI *TJ * LV)
     mpdata_fused_kernel(const __grid_constant__ CUtensorMap tm_pd,
                         const __grid_constant__ CUtensorMap tm_vn,
                         const __grid_constant__ CUtensorMap tm_wn,
                         const __grid_constant__ CUtensorMap tm_rho, const FusedArgs a) {
-    using C = FusedCfg<TI, TJ, KC, STAGES>;
+    using C = FusedCfg<TI, TJ, KC, STAGES, LV>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * C::kStageBytes);
 
     const int tid = threadIdx.x;
-    const int kl = tid & 15;    // level lane inside the chunk
-    const int vloc = tid >> 4;  // vertex inside the tile
+    const int kl = tid % LV;    // level lane inside the chunk
+    const int vloc = tid / LV;  // vertex inside the tile
     const int li = vloc / TJ, lj = vloc % TJ;
 
     // Stage-relative smem offsets (doubles) of this thread's point; fixed for the kernel.
@@ -163,6 +169,10 @@ __global__ void __launch_bounds__(TI *TJ * 16)
         for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if constexpr (OP == kComputeProbe) {  // benign operands: no slow-path divisions
+        double *d = reinterpret_cast<double *>(smem);
+        for (int q = tid; q < STAGES * C::kStageBytes / 8; q += blockDim.x) d[q] = 1.0 + 0.001 * (q & 7);
+    }
     __syncthreads();
 
     // producer cursor (thread 0 only), decoded once, then advanced incrementally
@@ -187,7 +197,8 @@ __global__ void __launch_bounds__(TI *TJ * 16)
         }
     };
     if (tid == 0) {
-        for (int s = 0; s < STAGES - 1 && s < n_units; ++s) issue_next(s);
+        if (OP != kComputeProbe)
+            for (int s = 0; s < STAGES - 1 && s < n_units; ++s) issue_next(s);
     }
 
     // consumer cursor
@@ -207,7 +218,7 @@ __global__ void __launch_bounds__(TI *TJ * 16)
         if (tid == 0 && n + STAGES - 1 < n_units) {
             // that stage was released by the __syncthreads() closing unit n-1
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_next((n + STAGES - 1) % STAGES);
+            if (OP != kComputeProbe) issue_next((n + STAGES - 1) % STAGES);
         }
         if (n == 0 || chunk == 0) {
             const int i = a.row_lo + ti * TI + li, j = tj * TJ + lj;
@@ -232,7 +243,7 @@ __global__ void __launch_bounds__(TI *TJ * 16)
             }
         }
 
-        mbar_wait(&bars[stage], (uint32_t)((n / STAGES) & 1));
+        if (OP != kComputeProbe) mbar_wait(&bars[stage], (uint32_t)((n / STAGES) & 1));
 
         const double *sp = reinterpret_cast<const double *>(smem + stage * C::kStageBytes + C::kPdOff) + oP;
         const double *sv = reinterpret_cast<const double *>(smem + stage * C::kStageBytes + C::kVnOff) + oV;
@@ -242,12 +253,18 @@ __global__ void __launch_bounds__(TI *TJ * 16)
 
 #pragma unroll
         for (int h = 0; h < C::kLevelsPerThread; ++h) {
-            const int kk = 16 * h;  // level offset of this pass inside the chunk
+            const int kk = LV * h;  // level offset of this pass inside the chunk
             const int k = k0 + kl + kk;
-            if (vvalid && k < a.K) {
+            if (vvalid && k < a.K && (KC % LV == 0 || kl + kk < KC)) {
                 const double *P = sp + kk;
                 const double *V = sv + kk;
                 const double p0 = P[0];
+                if constexpr (OP == kProbeOp) {
+                    // data-movement probe: touch the staged inputs, skip the arithmetic
+                    double *o = out + k;
+                    o[0] = add(add(p0, V[0]), add(sw[kk], sr[kk]));
+                    continue;
+                }
                 // the six incident edges in V->E slot order (connectivity.py:66); the
                 // origin is E->V slot 0 (connectivity.py:38-42)
                 const double f0 = edge_flux<OP>(p0, P[sPj], V[0]);
@@ -330,12 +347,12 @@ static int make_map(CUtensorMap *m, const double *ptr, int rank, const cuuint64_
 struct Variant {
     int ti, tj, kc, stages;
     int threads, smem;
-    void *fn[2];  // upwind, centred
+    void *fn[4];  // upwind, centred, data-movement probe, compute probe
 };
 
-template <int TI, int TJ, int KC, int STAGES>
+template <int TI, int TJ, int KC, int STAGES, int LV = 16>
 static Variant make_variant() {
-    using C = FusedCfg<TI, TJ, KC, STAGES>;
+    using C = FusedCfg<TI, TJ, KC, STAGES, LV>;
     Variant v;
     v.ti = TI;
     v.tj = TJ;
@@ -343,8 +360,10 @@ static Variant make_variant() {
     v.stages = STAGES;
     v.threads = C::kThreads;
     v.smem = C::kSmemBytes;
-    v.fn[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, TSG_UPWIND>;
-    v.fn[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, TSG_CENTRED>;
+    v.fn[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, TSG_UPWIND>;
+    v.fn[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, TSG_CENTRED>;
+    v.fn[2] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, kProbeOp>;
+    v.fn[3] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, kComputeProbe>;
     return v;
 }
 
@@ -358,6 +377,12 @@ static Variant *variants(int *count) {
         make_variant<8, 8, 16, 2>(),   // 6: 1024 threads, 2 stages
         make_variant<2, 32, 16, 3>(),  // 7: 1024 threads, long rows
         make_variant<4, 16, 16, 2>(),  // 8: 1024 threads, 2 stages
+        make_variant<4, 8, 32, 3, 32>(),   // 9: 1024 threads, a warp per vertex column
+        make_variant<2, 16, 32, 3, 32>(),  // 10: 1024 threads, a warp per vertex column
+        make_variant<2, 8, 80, 2, 16>(),   // 11: whole 80-level columns, 256 threads
+        make_variant<2, 8, 80, 2, 32>(),   // 12: whole 80-level columns, 512 threads
+        make_variant<4, 4, 80, 2, 32>(),   // 13: whole 80-level columns, 512 threads
+        make_variant<2, 8, 48, 2, 32>(),   // 14: 48-level chunks, 512 threads
     };
     *count = (int)(sizeof(v) / sizeof(v[0]));
     return v;
@@ -411,7 +436,8 @@ extern "C" int tsg_mpdata_step_rows(tsg_grid *g, const double *pd, const double 
     if (row_lo == row_hi) return TSG_OK;
     const int K = g->levels;
     if (K < 2) return fail(TSG_EVALUE, "the transport step needs at least 2 levels, got %d", K);
-    if (flux_op != TSG_UPWIND && flux_op != TSG_CENTRED)
+    if (flux_op != TSG_UPWIND && flux_op != TSG_CENTRED && flux_op != kProbeOp &&
+        flux_op != kComputeProbe)
         return fail(TSG_EVALUE, "flux operator must be one of ['centred', 'upwind'], got %d", flux_op);
     if (!pd || !vn || !wn || !rho || !signs || !dual || !pd_out)
         return fail(TSG_EVALUE, "tsg_mpdata_step: NULL array");
@@ -465,7 +491,7 @@ extern "C" int tsg_mpdata_step_rows(tsg_grid *g, const double *pd, const double 
     a.units = (int64_t)tiles_i * a.tiles_j * a.chunks;
     if (a.units >= (1LL << 31)) return fail(TSG_EVALUE, "patch too large for one fused launch");
 
-    void *fn = v.fn[flux_op];
+    void *fn = v.fn[flux_op == kProbeOp ? 2 : (flux_op == kComputeProbe ? 3 : flux_op)];
     TSG_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
     int per_sm = 0;
     TSG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, v.threads, v.smem));

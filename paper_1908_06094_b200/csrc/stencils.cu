@@ -9,207 +9,248 @@
 
 namespace tsg {
 
-static inline int grid_for(int64_t work, int threads, int num_sms) {
-    int64_t blocks = (work + threads - 1) / threads;
-    int64_t cap = (int64_t)num_sms * 16;
-    if (blocks > cap) blocks = cap;
-    return (int)(blocks < 1 ? 1 : blocks);
-}
-
-#define GRID_STRIDE(t, n)                                                     \
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (n); \
-         t += (int64_t)gridDim.x * blockDim.x)
-
-// t -> (i, c, j, k) over [rows][colors][cols][nk]
-struct Pt {
-    int i, c, j, k;
-};
-__device__ __forceinline__ Pt decompose(int64_t t, int nk, int cols, int colors) {
-    Pt p;
-    int64_t id = t / nk;
-    p.k = (int)(t - id * nk);
-    p.j = (int)(id % cols);
-    int64_t rest = id / cols;
-    p.c = (int)(rest % colors);
-    p.i = (int)(rest / colors);
-    return p;
-}
-
 // -- structured reduce over any relation (stencil.py:404-408 with the sum fold) -------
 
-__global__ void reduce_kernel(FieldIx Fs, FieldIx Fd, FieldIx Fsc, int rel, int nk,
-                              const double *__restrict__ src, const double *__restrict__ scale,
-                              double *__restrict__ dst, int flags) {
-    const int width = c_rel_width[rel];
-    const int64_t n = (int64_t)Fd.rows * Fd.colors * Fd.cols * nk;
-    GRID_STRIDE(t, n) {
-        Pt p = decompose(t, nk, Fd.cols, Fd.colors);
-        double acc = 0.0;
-        for (int s = 0; s < width; ++s) {
-            const int8_t *o = c_offsets[rel][p.c][s];
-            acc = add(src[Fs.at(p.i + o[0], o[1], p.j + o[2]) + p.k], acc);
+template <int REL, bool SCALE>
+__global__ void __launch_bounds__(256, 6) reduce_kernel(FieldIx Fs, FieldIx Fd, FieldIx Fsc, int nk,
+                                                     const double *__restrict__ src,
+                                                     const double *__restrict__ scale,
+                                                     double *__restrict__ dst, int flags) {
+    constexpr int W = REL < 3 ? 6 : (REL < 6 ? 3 : (REL == 8 ? 4 : 2));
+    TSG_LINES(Fd, i, c, j) {
+        const double *nb[W];
+#pragma unroll
+        for (int s = 0; s < W; ++s) {
+            const int8_t *o = c_offsets[REL][c][s];
+            nb[s] = src + Fs.at(i + o[0], o[1], j + o[2]);
         }
-        if (scale) acc = mul(acc, scale[Fsc.at(p.i, p.c, p.j)]);
-        store_img(dst, Fd, p.i, p.c, p.j, p.k, acc, flags);
+        const double sc = SCALE ? scale[Fsc.at(i, c, j)] : 1.0;
+        double *out = dst + Fd.at(i, c, j);
+        const Img m = images(Fd, i, j, flags);
+        for (int k = threadIdx.x; k < nk; k += 32) {
+            double acc = 0.0;
+#pragma unroll
+            for (int s = 0; s < W; ++s) acc = add(nb[s][k], acc);
+            if (SCALE) acc = mul(acc, sc);
+            put(out, m, k, acc);
+        }
     }
 }
 
 // -- table-driven reduce over flat arrays (kernels.py:83-104, reference.py:137-157) -----
 
-__global__ void reduce_indirect_kernel(const int64_t *__restrict__ table, int64_t nrows,
-                                       int width, int nlev, const double *__restrict__ src,
-                                       const double *__restrict__ scale,
-                                       double *__restrict__ dst) {
-    const int64_t n = nrows * nlev;
-    GRID_STRIDE(t, n) {
-        int64_t r = t / nlev;
-        int k = (int)(t - r * nlev);
-        double acc = 0.0;
-        for (int s = 0; s < width; ++s) acc = add(src[__ldg(table + r * width + s) * nlev + k], acc);
-        if (scale) acc = mul(acc, scale[r]);
-        dst[t] = acc;
+template <int W>
+__global__ void __launch_bounds__(256, 6) reduce_indirect_kernel(const int64_t *__restrict__ table,
+                                                              int64_t nrows, int width, int nlev,
+                                                              const double *__restrict__ src,
+                                                              const double *__restrict__ scale,
+                                                              double *__restrict__ dst) {
+    const int wd = W > 0 ? W : width;
+    for (int64_t r = (int64_t)blockIdx.x * kWarps + threadIdx.y; r < nrows;
+         r += (int64_t)gridDim.x * kWarps) {
+        const int64_t *row = table + r * wd;
+        const double sc = scale ? scale[r] : 1.0;
+        double *out = dst + r * nlev;
+        if (W > 0) {
+            const double *nb[W > 0 ? W : 1];
+#pragma unroll
+            for (int s = 0; s < W; ++s) nb[s] = src + __ldg(row + s) * nlev;
+            for (int k = threadIdx.x; k < nlev; k += 32) {
+                double acc = 0.0;
+#pragma unroll
+                for (int s = 0; s < W; ++s) acc = add(nb[s][k], acc);
+                out[k] = scale ? mul(acc, sc) : acc;
+            }
+        } else {
+            for (int k = threadIdx.x; k < nlev; k += 32) {
+                double acc = 0.0;
+                for (int s = 0; s < wd; ++s) acc = add(src[__ldg(row + s) * nlev + k], acc);
+                out[k] = scale ? mul(acc, sc) : acc;
+            }
+        }
     }
 }
 
 // -- cell divergence (mpdata.py:361-416, reference.py:119-134) --------------------------
 
-__global__ void cell_div_kernel(FieldIx Fvn, FieldIx Fl, FieldIx Fa, FieldIx Fw, FieldIx Fo,
-                                int nk, int weighted, const double *__restrict__ vn,
-                                const double *__restrict__ length,
-                                const double *__restrict__ area,
-                                const double *__restrict__ weights, double *__restrict__ out,
-                                int flags) {
-    const int rel = TSG_CELLS * 3 + TSG_EDGES;
-    const int64_t n = (int64_t)Fo.rows * 2 * Fo.cols * nk;
-    GRID_STRIDE(t, n) {
-        Pt p = decompose(t, nk, Fo.cols, 2);
-        double acc = 0.0;
+template <bool WEIGHTED>
+__global__ void __launch_bounds__(256, 6) cell_div_kernel(FieldIx Fvn, FieldIx Fl, FieldIx Fa,
+                                                       FieldIx Fw, FieldIx Fo, int nk,
+                                                       const double *__restrict__ vn,
+                                                       const double *__restrict__ length,
+                                                       const double *__restrict__ area,
+                                                       const double *__restrict__ weights,
+                                                       double *__restrict__ out, int flags) {
+    constexpr int REL = TSG_CELLS * 3 + TSG_EDGES;
+    TSG_LINES(Fo, i, c, j) {
+        const double *v[3];
+        double w[3];
+#pragma unroll
         for (int s = 0; s < 3; ++s) {
-            const int8_t *o = c_offsets[rel][p.c][s];
-            int ei = p.i + o[0], ec = o[1], ej = p.j + o[2];
-            double v = vn[Fvn.at(ei, ec, ej) + p.k];
-            double w = weighted ? weights[Fw.at(p.i, p.c, p.j) + s] : length[Fl.at(ei, ec, ej)];
-            acc = add(mul(v, w), acc);
+            const int8_t *o = c_offsets[REL][c][s];
+            v[s] = vn + Fvn.at(i + o[0], o[1], j + o[2]);
+            w[s] = WEIGHTED ? weights[Fw.at(i, c, j) + s] : length[Fl.at(i + o[0], o[1], j + o[2])];
         }
-        if (!weighted) acc = dvd(acc, area[Fa.at(p.i, p.c, p.j)]);
-        store_img(out, Fo, p.i, p.c, p.j, p.k, acc, flags);
+        const double a = WEIGHTED ? 1.0 : area[Fa.at(i, c, j)];
+        double *o = out + Fo.at(i, c, j);
+        const Img m = images(Fo, i, j, flags);
+        for (int k = threadIdx.x; k < nk; k += 32) {
+            double acc = 0.0;
+#pragma unroll
+            for (int s = 0; s < 3; ++s) acc = add(mul(v[s][k], w[s]), acc);
+            if (!WEIGHTED) acc = dvd(acc, a);
+            put(o, m, k, acc);
+        }
     }
 }
 
 // -- unfused MPDATA (run_naive analogue, executors.py:213-245) --------------------------
 
 template <int OP>
-__global__ void flux_kernel(FieldIx Fp, FieldIx Fe, int K, const double *__restrict__ pd,
-                            const double *__restrict__ vn, double *__restrict__ flux, int flags) {
-    const int64_t n = (int64_t)Fe.rows * 3 * Fe.cols * K;
-    GRID_STRIDE(t, n) {
-        Pt p = decompose(t, K, Fe.cols, 3);
+__global__ void __launch_bounds__(256, 6) flux_kernel(FieldIx Fp, FieldIx Fe, int K,
+                                                   const double *__restrict__ pd,
+                                                   const double *__restrict__ vn,
+                                                   double *__restrict__ flux, int flags) {
+    TSG_LINES(Fe, i, c, j) {
         // E->V slot 1 (connectivity.py:38-42): c0 (0,+1), c1 (+1,+1), c2 (+1,0)
-        int oi = p.c == 0 ? 0 : 1, oj = p.c == 2 ? 0 : 1;
-        double po = pd[Fp.at(p.i, 0, p.j) + p.k];
-        double pp = pd[Fp.at(p.i + oi, 0, p.j + oj) + p.k];
-        double v = vn[Fe.at(p.i, p.c, p.j) + p.k];
-        store_img(flux, Fe, p.i, p.c, p.j, p.k, edge_flux<OP>(po, pp, v), flags);
+        const double *po = pd + Fp.at(i, 0, j);
+        const double *pp = pd + Fp.at(i + (c == 0 ? 0 : 1), 0, j + (c == 2 ? 0 : 1));
+        const double *v = vn + Fe.at(i, c, j);
+        double *o = flux + Fe.at(i, c, j);
+        const Img m = images(Fe, i, j, flags);
+        for (int k = threadIdx.x; k < K; k += 32) put(o, m, k, edge_flux<OP>(po[k], pp[k], v[k]));
     }
 }
 
-__global__ void fluz_kernel(FieldIx Fp, FieldIx Fw, int K, double pivbz,
-                            const double *__restrict__ pd, const double *__restrict__ wn,
-                            double *__restrict__ fluz, int flags) {
-    const int64_t n = (int64_t)Fp.rows * Fp.cols * (K + 1);
-    GRID_STRIDE(t, n) {
-        Pt p = decompose(t, K + 1, Fp.cols, 1);
-        const double *P = pd + Fp.at(p.i, 0, p.j);
-        const double *W = wn + Fw.at(p.i, 0, p.j);
-        double f;
-        if (p.k == 0) f = mul(pivbz, fluz_interior(W[1], P[0], P[1]));
-        else if (p.k == K) f = mul(pivbz, fluz_interior(W[K - 1], P[K - 2], P[K - 1]));
-        else f = fluz_interior(W[p.k], P[p.k - 1], P[p.k]);
-        store_img(fluz, Fw, p.i, 0, p.j, p.k, f, flags);
-    }
-}
-
-__global__ void div_kernel(FieldIx Fe, FieldIx Fw, FieldIx Fs, FieldIx Fd, FieldIx Fv, int K,
-                           const double *__restrict__ flux, const double *__restrict__ fluz,
-                           const double *__restrict__ signs, const double *__restrict__ dual,
-                           double *__restrict__ divvd, int flags) {
-    const int rel = TSG_VERTICES * 3 + TSG_EDGES;
-    const int64_t n = (int64_t)Fv.rows * Fv.cols * K;
-    GRID_STRIDE(t, n) {
-        Pt p = decompose(t, K, Fv.cols, 1);
-        const double *S = signs + Fs.at(p.i, 0, p.j);
-        double acc = 0.0;
-        for (int s = 0; s < 6; ++s) {
-            const int8_t *o = c_offsets[rel][0][s];
-            acc = add(mul(S[s], flux[Fe.at(p.i + o[0], o[1], p.j + o[2]) + p.k]), acc);
+__global__ void __launch_bounds__(256, 6) fluz_kernel(FieldIx Fp, FieldIx Fw, int K, double pivbz,
+                                                   const double *__restrict__ pd,
+                                                   const double *__restrict__ wn,
+                                                   double *__restrict__ fluz, int flags) {
+    TSG_LINES(Fp, i, c, j) {
+        const double *P = pd + Fp.at(i, 0, j);
+        const double *W = wn + Fw.at(i, 0, j);
+        double *o = fluz + Fw.at(i, 0, j);
+        const Img m = images(Fw, i, j, flags);
+        for (int k = threadIdx.x; k <= K; k += 32) {
+            double f;
+            if (k == 0) f = mul(pivbz, fluz_interior(W[1], P[0], P[1]));
+            else if (k == K) f = mul(pivbz, fluz_interior(W[K - 1], P[K - 2], P[K - 1]));
+            else f = fluz_interior(W[k], P[k - 1], P[k]);
+            put(o, m, k, f);
         }
-        const double *Z = fluz + Fw.at(p.i, 0, p.j);
-        acc = add(acc, sub(Z[p.k + 1], Z[p.k]));
-        store_img(divvd, Fv, p.i, 0, p.j, p.k, dvd(acc, dual[Fd.at(p.i, 0, p.j)]), flags);
     }
 }
 
-__global__ void advance_kernel(FieldIx Fv, int K, double dt, const double *__restrict__ pd,
-                               const double *__restrict__ divvd, const double *__restrict__ rho,
-                               double *__restrict__ pd_out, int flags) {
-    const int64_t n = (int64_t)Fv.rows * Fv.cols * K;
-    GRID_STRIDE(t, n) {
-        Pt p = decompose(t, K, Fv.cols, 1);
-        int64_t o = Fv.at(p.i, 0, p.j) + p.k;
-        double slope = mul(dt, divvd[o]);
-        slope = dvd(slope, rho[o]);
-        store_img(pd_out, Fv, p.i, 0, p.j, p.k, sub(pd[o], slope), flags);
+__global__ void __launch_bounds__(256, 6) div_kernel(FieldIx Fe, FieldIx Fw, FieldIx Fs, FieldIx Fd,
+                                                  FieldIx Fv, int K, const double *__restrict__ flux,
+                                                  const double *__restrict__ fluz,
+                                                  const double *__restrict__ signs,
+                                                  const double *__restrict__ dual,
+                                                  double *__restrict__ divvd, int flags) {
+    constexpr int REL = TSG_VERTICES * 3 + TSG_EDGES;
+    TSG_LINES(Fv, i, c, j) {
+        const double *f[6];
+        double sg[6];
+        const double *S = signs + Fs.at(i, 0, j);
+#pragma unroll
+        for (int s = 0; s < 6; ++s) {
+            const int8_t *o = c_offsets[REL][0][s];
+            f[s] = flux + Fe.at(i + o[0], o[1], j + o[2]);
+            sg[s] = S[s];
+        }
+        const double *Z = fluz + Fw.at(i, 0, j);
+        const double du = dual[Fd.at(i, 0, j)];
+        double *o = divvd + Fv.at(i, 0, j);
+        const Img m = images(Fv, i, j, flags);
+        for (int k = threadIdx.x; k < K; k += 32) {
+            double acc = 0.0;
+#pragma unroll
+            for (int s = 0; s < 6; ++s) acc = add(mul(sg[s], f[s][k]), acc);
+            acc = add(acc, sub(Z[k + 1], Z[k]));
+            put(o, m, k, dvd(acc, du));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256, 6) advance_kernel(FieldIx Fv, int K, double dt,
+                                                      const double *__restrict__ pd,
+                                                      const double *__restrict__ divvd,
+                                                      const double *__restrict__ rho,
+                                                      double *__restrict__ pd_out, int flags) {
+    TSG_LINES(Fv, i, c, j) {
+        const int64_t e = Fv.at(i, 0, j);
+        const Img m = images(Fv, i, j, flags);
+        for (int k = threadIdx.x; k < K; k += 32) {
+            double slope = mul(dt, divvd[e + k]);
+            slope = dvd(slope, rho[e + k]);
+            put(pd_out + e, m, k, sub(pd[e + k], slope));
+        }
     }
 }
 
 // -- indirect (table-driven) MPDATA over flat arrays (reference.py:93-116) -------------
 
+#define TSG_FLAT_ROWS(r, n)                                                          \
+    for (int64_t r = (int64_t)blockIdx.x * kWarps + threadIdx.y; r < (n);          \
+         r += (int64_t)gridDim.x * kWarps)
+
 template <int OP>
-__global__ void iflux_kernel(const int64_t *__restrict__ e2v, int64_t ne, int K,
-                             const double *__restrict__ pd, const double *__restrict__ vn,
-                             double *__restrict__ flux) {
-    GRID_STRIDE(t, ne * K) {
-        int64_t e = t / K;
-        int k = (int)(t - e * K);
-        double po = pd[__ldg(e2v + 2 * e) * K + k], pp = pd[__ldg(e2v + 2 * e + 1) * K + k];
-        flux[t] = edge_flux<OP>(po, pp, vn[t]);
+__global__ void __launch_bounds__(256, 6) iflux_kernel(const int64_t *__restrict__ e2v, int64_t ne,
+                                                    int K, const double *__restrict__ pd,
+                                                    const double *__restrict__ vn,
+                                                    double *__restrict__ flux) {
+    TSG_FLAT_ROWS(e, ne) {
+        const double *po = pd + __ldg(e2v + 2 * e) * K, *pp = pd + __ldg(e2v + 2 * e + 1) * K;
+        const double *v = vn + e * K;
+        double *o = flux + e * K;
+        for (int k = threadIdx.x; k < K; k += 32) o[k] = edge_flux<OP>(po[k], pp[k], v[k]);
     }
 }
 
-__global__ void ifluz_kernel(int64_t nv, int K, double pivbz, const double *__restrict__ pd,
-                             const double *__restrict__ wn, double *__restrict__ fluz) {
-    GRID_STRIDE(t, nv * (K + 1)) {
-        int64_t v = t / (K + 1);
-        int k = (int)(t - v * (K + 1));
+__global__ void __launch_bounds__(256, 6) ifluz_kernel(int64_t nv, int K, double pivbz,
+                                                    const double *__restrict__ pd,
+                                                    const double *__restrict__ wn,
+                                                    double *__restrict__ fluz) {
+    TSG_FLAT_ROWS(v, nv) {
         const double *P = pd + v * K, *W = wn + v * (K + 1);
-        double f;
-        if (k == 0) f = mul(pivbz, fluz_interior(W[1], P[0], P[1]));
-        else if (k == K) f = mul(pivbz, fluz_interior(W[K - 1], P[K - 2], P[K - 1]));
-        else f = fluz_interior(W[k], P[k - 1], P[k]);
-        fluz[t] = f;
+        double *o = fluz + v * (K + 1);
+        for (int k = threadIdx.x; k <= K; k += 32) {
+            double f;
+            if (k == 0) f = mul(pivbz, fluz_interior(W[1], P[0], P[1]));
+            else if (k == K) f = mul(pivbz, fluz_interior(W[K - 1], P[K - 2], P[K - 1]));
+            else f = fluz_interior(W[k], P[k - 1], P[k]);
+            o[k] = f;
+        }
     }
 }
 
-__global__ void idiv_advance_kernel(const int64_t *__restrict__ v2e, int64_t nv, int K, double dt,
-                                    const double *__restrict__ signs,
-                                    const double *__restrict__ dual,
-                                    const double *__restrict__ flux,
-                                    const double *__restrict__ fluz,
-                                    const double *__restrict__ pd, const double *__restrict__ rho,
-                                    double *__restrict__ div, double *__restrict__ pd_out) {
-    GRID_STRIDE(t, nv * K) {
-        int64_t v = t / K;
-        int k = (int)(t - v * K);
-        double acc = 0.0;
-        for (int s = 0; s < 6; ++s)
-            acc = add(mul(__ldg(signs + v * 6 + s), flux[__ldg(v2e + v * 6 + s) * K + k]), acc);
+__global__ void __launch_bounds__(256, 6) idiv_advance_kernel(
+    const int64_t *__restrict__ v2e, int64_t nv, int K, double dt, const double *__restrict__ signs,
+    const double *__restrict__ dual, const double *__restrict__ flux,
+    const double *__restrict__ fluz, const double *__restrict__ pd, const double *__restrict__ rho,
+    double *__restrict__ div, double *__restrict__ pd_out) {
+    TSG_FLAT_ROWS(v, nv) {
+        const double *f[6];
+        double sg[6];
+#pragma unroll
+        for (int s = 0; s < 6; ++s) {
+            f[s] = flux + __ldg(v2e + v * 6 + s) * K;
+            sg[s] = __ldg(signs + v * 6 + s);
+        }
         const double *Z = fluz + v * (K + 1);
-        acc = add(acc, sub(Z[k + 1], Z[k]));
-        double d = dvd(acc, __ldg(dual + v));
-        div[t] = d;
-        double slope = mul(dt, d);
-        slope = dvd(slope, rho[t]);
-        pd_out[t] = sub(pd[t], slope);
+        const double du = __ldg(dual + v);
+        const int64_t e = v * K;
+        for (int k = threadIdx.x; k < K; k += 32) {
+            double acc = 0.0;
+#pragma unroll
+            for (int s = 0; s < 6; ++s) acc = add(mul(sg[s], f[s][k]), acc);
+            acc = add(acc, sub(Z[k + 1], Z[k]));
+            const double d = dvd(acc, du);
+            div[e + k] = d;
+            double slope = mul(dt, d);
+            slope = dvd(slope, rho[e + k]);
+            pd_out[e + k] = sub(pd[e + k], slope);
+        }
     }
 }
 
@@ -235,9 +276,22 @@ extern "C" int tsg_neighbor_reduce(const tsg_grid *g, int from_loc, int to_loc, 
     FieldIx Fs(g->rows, g->cols, colors_of(to_loc), inner);
     FieldIx Fd(g->rows, g->cols, colors_of(from_loc), inner);
     FieldIx Fsc(g->rows, g->cols, colors_of(from_loc), 1);
-    int64_t n = (int64_t)g->rows * Fd.colors * g->cols * inner;
-    reduce_kernel<<<grid_for(n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(
-        Fs, Fd, Fsc, from_loc * 3 + to_loc, inner, src, scale, dst, g->flags);
+    const dim3 grid = line_grid(g->cols, (int64_t)g->rows * Fd.colors, g->num_sms), block = line_block();
+    cudaStream_t st = (cudaStream_t)s;
+    const int rel = from_loc * 3 + to_loc;
+#define TSG_REDUCE_CASE(R)                                                                          \
+    case R:                                                                                        \
+        if (scale)                                                                                 \
+            reduce_kernel<R, true><<<grid, block, 0, st>>>(Fs, Fd, Fsc, inner, src, scale, dst, g->flags); \
+        else                                                                                       \
+            reduce_kernel<R, false><<<grid, block, 0, st>>>(Fs, Fd, Fsc, inner, src, scale, dst, g->flags); \
+        break;
+    switch (rel) {
+        TSG_REDUCE_CASE(0) TSG_REDUCE_CASE(1) TSG_REDUCE_CASE(2) TSG_REDUCE_CASE(3)
+        TSG_REDUCE_CASE(4) TSG_REDUCE_CASE(5) TSG_REDUCE_CASE(6) TSG_REDUCE_CASE(7)
+        TSG_REDUCE_CASE(8)
+    }
+#undef TSG_REDUCE_CASE
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }
@@ -249,8 +303,15 @@ extern "C" int tsg_neighbor_reduce_indirect(const int64_t *table, int64_t nrows,
     if (nrows < 0 || width < 1 || nlev < 1)
         return fail(TSG_EVALUE, "bad table shape (%lld, %d) / levels %d", (long long)nrows, width, nlev);
     if (nrows == 0) return TSG_OK;
-    reduce_indirect_kernel<<<grid_for(nrows * nlev, 256, sm_count()), 256, 0, (cudaStream_t)s>>>(
-        table, nrows, width, nlev, src, scale, dst);
+    const int nb = flat_blocks(nrows, sm_count());
+    cudaStream_t st = (cudaStream_t)s;
+    switch (width) {
+        case 2: reduce_indirect_kernel<2><<<nb, line_block(), 0, st>>>(table, nrows, width, nlev, src, scale, dst); break;
+        case 3: reduce_indirect_kernel<3><<<nb, line_block(), 0, st>>>(table, nrows, width, nlev, src, scale, dst); break;
+        case 4: reduce_indirect_kernel<4><<<nb, line_block(), 0, st>>>(table, nrows, width, nlev, src, scale, dst); break;
+        case 6: reduce_indirect_kernel<6><<<nb, line_block(), 0, st>>>(table, nrows, width, nlev, src, scale, dst); break;
+        default: reduce_indirect_kernel<0><<<nb, line_block(), 0, st>>>(table, nrows, width, nlev, src, scale, dst);
+    }
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }
@@ -264,9 +325,13 @@ extern "C" int tsg_cell_divergence(const tsg_grid *g, int weighted, const double
     int K = g->levels;
     FieldIx Fvn(g->rows, g->cols, 3, K), Fl(g->rows, g->cols, 3, 1), Fa(g->rows, g->cols, 2, 1),
         Fw(g->rows, g->cols, 2, 3), Fo(g->rows, g->cols, 2, K);
-    int64_t n = (int64_t)g->rows * 2 * g->cols * K;
-    cell_div_kernel<<<grid_for(n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(
-        Fvn, Fl, Fa, Fw, Fo, K, weighted, vn, length, area, weights, out, g->flags);
+    const dim3 grid = line_grid(g->cols, 2LL * g->rows, g->num_sms);
+    if (weighted)
+        cell_div_kernel<true><<<grid, line_block(), 0, (cudaStream_t)s>>>(
+            Fvn, Fl, Fa, Fw, Fo, K, vn, length, area, weights, out, g->flags);
+    else
+        cell_div_kernel<false><<<grid, line_block(), 0, (cudaStream_t)s>>>(
+            Fvn, Fl, Fa, Fw, Fo, K, vn, length, area, weights, out, g->flags);
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }
@@ -291,17 +356,14 @@ extern "C" int tsg_mpdata_step_unfused(const tsg_grid *g, const double *pd, cons
     cudaStream_t st = (cudaStream_t)s;
     FieldIx Fv(g->rows, g->cols, 1, K), Fe(g->rows, g->cols, 3, K), Fw(g->rows, g->cols, 1, K + 1),
         Fs(g->rows, g->cols, 1, 6), Fd(g->rows, g->cols, 1, 1);
-    const int T = 256, sms = g->num_sms;
-    int64_t nE = (int64_t)g->rows * 3 * g->cols * K, nV = (int64_t)g->rows * g->cols * K;
+    const dim3 gE = line_grid(g->cols, 3LL * g->rows, g->num_sms), gV = line_grid(g->cols, g->rows, g->num_sms), b = line_block();
     if (flux_op == TSG_UPWIND)
-        flux_kernel<TSG_UPWIND><<<grid_for(nE, T, sms), T, 0, st>>>(Fv, Fe, K, pd, vn, flux, g->flags);
+        flux_kernel<TSG_UPWIND><<<gE, b, 0, st>>>(Fv, Fe, K, pd, vn, flux, g->flags);
     else
-        flux_kernel<TSG_CENTRED><<<grid_for(nE, T, sms), T, 0, st>>>(Fv, Fe, K, pd, vn, flux, g->flags);
-    fluz_kernel<<<grid_for(nV + g->rows * (int64_t)g->cols, T, sms), T, 0, st>>>(Fv, Fw, K, pivbz,
-                                                                               pd, wn, fluz, g->flags);
-    div_kernel<<<grid_for(nV, T, sms), T, 0, st>>>(Fe, Fw, Fs, Fd, Fv, K, flux, fluz, signs, dual,
-                                                  divvd, g->flags);
-    advance_kernel<<<grid_for(nV, T, sms), T, 0, st>>>(Fv, K, dt, pd, divvd, rho, pd_out, g->flags);
+        flux_kernel<TSG_CENTRED><<<gE, b, 0, st>>>(Fv, Fe, K, pd, vn, flux, g->flags);
+    fluz_kernel<<<gV, b, 0, st>>>(Fv, Fw, K, pivbz, pd, wn, fluz, g->flags);
+    div_kernel<<<gV, b, 0, st>>>(Fe, Fw, Fs, Fd, Fv, K, flux, fluz, signs, dual, divvd, g->flags);
+    advance_kernel<<<gV, b, 0, st>>>(Fv, K, dt, pd, divvd, rho, pd_out, g->flags);
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }
@@ -317,14 +379,15 @@ extern "C" int tsg_transport_indirect(const int64_t *e2v, const int64_t *v2e, co
         return fail(TSG_EVALUE, "tsg_transport_indirect: NULL array");
     if (nv < 1 || ne < 1) return fail(TSG_EVALUE, "empty mesh (nv=%lld, ne=%lld)", (long long)nv, (long long)ne);
     cudaStream_t st = (cudaStream_t)s;
-    const int T = 256, sms = sm_count();
+    const int sms = sm_count();
+    const dim3 b = line_block();
     if (flux_op == TSG_UPWIND)
-        iflux_kernel<TSG_UPWIND><<<grid_for(ne * nlev, T, sms), T, 0, st>>>(e2v, ne, nlev, pd, vn, flux);
+        iflux_kernel<TSG_UPWIND><<<flat_blocks(ne, sms), b, 0, st>>>(e2v, ne, nlev, pd, vn, flux);
     else
-        iflux_kernel<TSG_CENTRED><<<grid_for(ne * nlev, T, sms), T, 0, st>>>(e2v, ne, nlev, pd, vn, flux);
-    ifluz_kernel<<<grid_for(nv * (nlev + 1), T, sms), T, 0, st>>>(nv, nlev, pivbz, pd, wn, fluz);
-    idiv_advance_kernel<<<grid_for(nv * nlev, T, sms), T, 0, st>>>(v2e, nv, nlev, dt, signs, dual,
-                                                                  flux, fluz, pd, rho, div, pd_out);
+        iflux_kernel<TSG_CENTRED><<<flat_blocks(ne, sms), b, 0, st>>>(e2v, ne, nlev, pd, vn, flux);
+    ifluz_kernel<<<flat_blocks(nv, sms), b, 0, st>>>(nv, nlev, pivbz, pd, wn, fluz);
+    idiv_advance_kernel<<<flat_blocks(nv, sms), b, 0, st>>>(v2e, nv, nlev, dt, signs, dual, flux, fluz,
+                                                           pd, rho, div, pd_out);
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }

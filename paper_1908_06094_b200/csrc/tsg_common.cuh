@@ -58,6 +58,60 @@ struct FieldIx {
     __host__ __device__ int64_t elems() const { return (int64_t)(rows + 2) * rowstr; }
 };
 
+// Division by a run-time invariant divisor in three instructions (Granlund & Montgomery,
+// "Division by invariant integers using multiplication", 1994, fig. 4.1): valid for every
+// 32-bit n.  Element/level decompositions of the streaming kernels use it instead of
+// 64-bit integer division.
+struct FastDiv {
+    uint32_t d, m, s;
+    __host__ __device__ FastDiv() : d(1), m(0), s(0) {}
+    __host__ explicit FastDiv(uint32_t div) : d(div), m(0), s(0) {
+        if (d <= 1) return;
+        uint32_t l = 0;
+        while ((1ull << l) < d) ++l;  // ceil(log2 d)
+        m = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+        s = l;
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        if (d == 1) return n;
+        const uint32_t t = __umulhi(n, m);
+        return (t + ((n - t) >> 1)) >> (s - 1);
+    }
+};
+
+// (element, level) decomposition of a flat point index t = ((i*colors + c)*cols + j)*nk + k.
+struct PointDec {
+    FastDiv nk, cols, colors;
+    uint32_t n;  // number of points (< 2^32)
+    __host__ PointDec() {}
+    __host__ PointDec(int64_t rows, int ncols, int ncolors, int nlev)
+        : nk(nlev), cols(ncols), colors(ncolors), n((uint32_t)(rows * ncolors * ncols * nlev)) {}
+    static bool fits(int64_t rows, int ncols, int ncolors, int nlev) {
+        return rows * ncolors * ncols * nlev < (1LL << 32) - (1LL << 24);
+    }
+};
+
+struct Pt {
+    int i, c, j, k;
+    uint32_t e;  // canonical element id
+};
+
+__device__ __forceinline__ Pt decompose(uint32_t t, const PointDec &D) {
+    Pt p;
+    p.e = D.nk.div(t);
+    p.k = (int)(t - p.e * D.nk.d);
+    const uint32_t rest = D.cols.div(p.e);
+    p.j = (int)(p.e - rest * D.cols.d);
+    const uint32_t i = D.colors.div(rest);
+    p.c = (int)(rest - i * D.colors.d);
+    p.i = (int)i;
+    return p;
+}
+
+#define TSG_POINTS(t, D)                                                             \
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < (D).n;             \
+         t += gridDim.x * blockDim.x)
+
 // Store `v` at interior (i, c, j, k) and at every periodic halo image of it.
 __device__ __forceinline__ void store_img(double *f, const FieldIx &F, int i, int c, int j,
                                           int k, double v, int flags) {
@@ -76,6 +130,59 @@ __device__ __forceinline__ void store_img(double *f, const FieldIx &F, int i, in
     if (ri != -2 && cj != -2) f[F.at(ri, c, cj) + k] = v;
 }
 
+// Launch geometry of the element-line kernels: one warp per element, lanes along the
+// contiguous level run (coalesced 256-byte accesses), 8 elements (warps) per block along j,
+// one block row per (row, colour) line.  Neighbour pointers, periodic-image offsets and
+// table rows are resolved once per element and reused for every level.
+constexpr int kWarps = 8;
+
+inline dim3 line_grid(int cols, int64_t lines, int num_sms = 148) {
+    // enough blocks for 8 resident blocks (2048 threads) per SM; each block then walks
+    // several (row, colour) lines, so short kernels are not dominated by block launches
+    const int64_t gx = (cols + kWarps - 1) / kWarps;
+    int64_t gy = ((int64_t)num_sms * 8 + gx - 1) / gx;
+    if (gy > lines) gy = lines;
+    if (gy > 65535) gy = 65535;
+    return dim3((unsigned)gx, (unsigned)(gy < 1 ? 1 : gy));
+}
+inline dim3 line_block() { return dim3(32, kWarps); }
+
+inline int flat_blocks(int64_t rows, int num_sms) {
+    int64_t b = (rows + kWarps - 1) / kWarps, cap = (int64_t)num_sms * 32;
+    return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+#define TSG_LINES(F, i, c, j)                                                              \
+    const int j = blockIdx.x * kWarps + threadIdx.y;                                       \
+    if (j >= (F).cols) return;                                                             \
+    for (int line_ = blockIdx.y; line_ < (F).rows * (F).colors; line_ += gridDim.y)        \
+        for (int i = line_ / (F).colors, c = line_ - i * (F).colors, once_ = 1; once_; once_ = 0)
+
+// offsets of the periodic halo images of element (i, j) (0 = none)
+struct Img {
+    int64_t dr, dc;
+};
+__device__ __forceinline__ Img images(const FieldIx &F, int i, int j, int flags) {
+    Img m{0, 0};
+    if (flags & TSG_PERIODIC_ROWS) {
+        if (i == 0) m.dr = (int64_t)F.rows * F.rowstr;
+        else if (i == F.rows - 1) m.dr = -(int64_t)F.rows * F.rowstr;
+    }
+    if (flags & TSG_PERIODIC_COLS) {
+        if (j == 0) m.dc = (int64_t)F.cols * F.cstride;
+        else if (j == F.cols - 1) m.dc = -(int64_t)F.cols * F.cstride;
+    }
+    return m;
+}
+__device__ __forceinline__ void put(double *o, const Img &m, int k, double v) {
+    o[k] = v;
+    if (m.dr | m.dc) {
+        if (m.dr) o[m.dr + k] = v;
+        if (m.dc) o[m.dc + k] = v;
+        if (m.dr && m.dc) o[m.dr + m.dc + k] = v;
+    }
+}
+
 // numpy.maximum(a, 0.0) / numpy.minimum(a, 0.0): NaN in `a` propagates, ties return
 // the second operand (+0.0) -- measured numpy 2.3 semantics, SURVEY Appendix A.
 __device__ __forceinline__ double npmax0(double a) { return (a > 0.0 || a != a) ? a : 0.0; }
@@ -91,7 +198,7 @@ __device__ __forceinline__ double dvd(double a, double b) { return __ddiv_rn(a, 
 // mpdata.py:189-199 / reference.py:18-35
 template <int OP>
 __device__ __forceinline__ double edge_flux(double p_origin, double p_other, double vn) {
-    if (OP == TSG_UPWIND) return add(mul(p_origin, npmax0(vn)), mul(p_other, npmin0(vn)));
+    if (OP != TSG_CENTRED) return add(mul(p_origin, npmax0(vn)), mul(p_other, npmin0(vn)));
     return mul(mul(0.5, vn), add(p_origin, p_other));
 }
 // reference.py:52-56: max(w,0)*pd(k-1) + min(w,0)*pd(k)

@@ -273,9 +273,11 @@ def test_every_fused_variant_is_bitwise_identical(cuda_ok):
     inp = O.transport_inputs(r, c, lev, 4, "random", "random", "random")
     want = O.step_inputs(r, c, inp, 0.2, 0.8)["pd_out"]
     try:
-        for v in range(1, 9):
+        v = 1
+        while _lib.lib().tsg_fused_variant_info(v, *[None] * 6) == 0:
             _lib.call("tsg_set_fused_variant", v)
             assert np.array_equal(fused_step(r, c, lev, inp, 0.2, 0.8), want), v
+            v += 1
     finally:
         _lib.call("tsg_set_fused_variant", 0)
 
