@@ -197,6 +197,67 @@ class StructuredStepper:
         out.copy_(self.out_buf, non_blocking=True)
         return out
 
+    def run_pipelined(self, inputs, outputs, dt, pivbz, flux_op="upwind"):
+        """Many independent host-fed steps with copies overlapped (PCIe is full duplex).
+
+        ``inputs[n]`` = (pd, vn, wn, rho) pinned host tensors of step n, ``outputs[n]`` a
+        pinned host tensor receiving that step's pd_out.  Three streams: the H2D copy of
+        step n+1 runs while step n is reordered / advanced on the GPU and step n-1's result
+        is copied back; flat staging buffers are double-buffered and guarded by events.
+        Returns (start_event, end_event) bracketing all the work.
+        """
+        import torch
+
+        K = self.spec.levels
+        if not hasattr(self, "_pipe"):
+            dev = self.grid.device
+            self._pipe = {
+                "h2d": torch.cuda.Stream(), "comp": torch.cuda.Stream(), "d2h": torch.cuda.Stream(),
+                "in": [{k: torch.empty_like(v) for k, v in self.in_bufs.items()} for _ in range(2)],
+                "out": [torch.empty_like(self.out_buf) for _ in range(2)],
+            }
+        P = self._pipe
+        ev = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(P["h2d"])
+        packed = [None, None]    # staging set b free again (its pack kernels finished)
+        fetched = [None, None]   # output buffer b free again (its D2H finished)
+        last = None
+        for n, (src, dst) in enumerate(zip(inputs, outputs)):
+            b = n % 2
+            h2d, comp, d2h = P["h2d"], P["comp"], P["d2h"]
+            if packed[b] is not None:
+                h2d.wait_event(packed[b])
+            with torch.cuda.stream(h2d):
+                for k, t in zip(("pd", "vn", "wn", "rho"), src):
+                    P["in"][b][k].copy_(t, non_blocking=True)
+            landed = ev()
+            landed.record(h2d)
+            comp.wait_event(landed)
+            ib = P["in"][b]
+            self._pack(0, K, ib["pd"], self.fwd_v, self.pd, comp)
+            self._pack(2, K, ib["vn"], self.fwd_e, self.vn, comp)
+            self._pack(0, K + 1, ib["wn"], self.fwd_v, self.wn, comp)
+            self._pack(0, K, ib["rho"], self.fwd_v, self.rho, comp)
+            packed[b] = ev()
+            packed[b].record(comp)
+            self.step(dt, pivbz, flux_op, stream=comp)
+            if fetched[b] is not None:
+                comp.wait_event(fetched[b])
+            _lib.call("tsg_unpack", self.grid.handle, 0, K, _lib.ptr(self.pd_out), _lib.ptr(self.fwd_v),
+                      _lib.ptr(P["out"][b]), _lib.stream_handle(comp))
+            ready = ev()
+            ready.record(comp)
+            d2h.wait_event(ready)
+            with torch.cuda.stream(d2h):
+                dst.copy_(P["out"][b], non_blocking=True)
+            fetched[b] = ev()
+            fetched[b].record(d2h)
+            last = fetched[b]
+        P["d2h"].wait_event(last)
+        end.record(P["d2h"])
+        return start, end
+
     def __call__(self, pd, vn, wn, rho, dt, pivbz, flux_op="upwind"):
         self.upload(pd, vn, wn, rho)
         self.step(dt, pivbz, flux_op)

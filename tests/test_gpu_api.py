@@ -335,3 +335,28 @@ def test_fill_hash_is_decomposition_invariant(cuda_ok):
         t = strip.empty(2, 5)
         _lib.call("tsg_fill_hash", strip.handle, 2, 5, 7, -1.0, 1.0, _lib.ptr(t), s)
         assert np.array_equal(t[1:nr + 1].cpu().numpy(), f[r0 + 1:r0 + nr + 1].cpu().numpy())
+
+
+def test_pipelined_host_fed_steps_match_oracle(cuda_ok):
+    """StructuredStepper.run_pipelined (the e2e path of bench.py): three different host input
+    sets streamed with overlapped H2D / compute / D2H give the oracle's results bitwise."""
+    import torch
+
+    r, c, lev = 23, 31, 12
+    spec = T.PatchSpec(r, c, lev)
+    st = T.StructuredStepper(spec)
+    sets, want = [], []
+    for seed in range(3):
+        inp = O.transport_inputs(r, c, lev, seed, "random", "random", "random")
+        if seed == 0:
+            st.set_geometry(inp["signs"], inp["dual"])
+            geo = inp
+        else:
+            inp.update(signs=geo["signs"], dual=geo["dual"])
+        sets.append([torch.from_numpy(inp[n]).pin_memory() for n in ("pd", "vn", "wn", "rho")])
+        want.append(O.step_inputs(r, c, inp, 0.2, 0.8)["pd_out"])
+    outs = [torch.empty((r * c, lev), dtype=torch.float64).pin_memory() for _ in range(3)]
+    st.run_pipelined(sets, outs, 0.2, 0.8)
+    torch.cuda.synchronize()
+    for o, w in zip(outs, want):
+        assert np.array_equal(o.numpy(), w)
