@@ -211,7 +211,7 @@ def run_ours(args):
     if not host_fed:
         from paper_1908_06094_b200.distributed import StripStepper
 
-        stepper = StripStepper(global_rows, cols, K, rank, world, seed=0)
+        stepper = StripStepper(global_rows, cols, K, rank, world, seed=0, mode=args.exchange)
         my_rows = stepper.nrows
     else:
         my_rows = ROWS
@@ -251,6 +251,7 @@ def run_ours(args):
         t_wall = time.perf_counter() - t_wall0
     if not host_fed:
         stepper.finish()
+        stepper.check()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_s = sum(step_ms) / 1e3
     if world > 1:
@@ -321,6 +322,9 @@ def run_ours(args):
         "config": {"workload": w["label"], "rows": global_rows, "cols": cols, "levels": K,
                    "rows_per_gpu": my_rows, "vertices": GV, "edges": 3 * GV,
                    "dt": DT, "pivbz": PIVBZ, "parallelism": f"row-strips x{world}",
+                   "halo_exchange": ("none" if world == 1 else
+                                     "fused P2P stores from the step epilogue (CUDA IPC over NVLink)"
+                                     if args.exchange == "p2p" else "NCCL grouped send/recv"),
                    "l2": "256 MiB read-only L2 flush before every timed step (outside the events)",
                    "fused_tile": {"ti": vi[0].value, "tj": vi[1].value, "kc": vi[2].value,
                                   "stages": vi[3].value, "threads": vi[4].value,
@@ -351,6 +355,8 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--variant", type=int, default=0, help="fused tile variant (0 = default)")
+    ap.add_argument("--exchange", choices=("p2p", "nccl"), default="p2p",
+                    help="N>1 halo exchange: fused P2P epilogue stores (default) or NCCL send/recv")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3",
                     help="cfg3 (headline, weak scaling) or o1280 (strong scaling)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

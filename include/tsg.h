@@ -114,6 +114,15 @@ int tsg_mpdata_step_rows(tsg_grid *g, const double *pd, const double *vn, const 
                          const double *rho, const double *signs, const double *dual,
                          double *pd_out, double dt, double pivbz, int flux_op, int row_lo,
                          int row_hi, tsg_stream s);
+/* Row-strip step with the halo exchange fused into the epilogue: this strip's first row
+ * is also stored into `halo_up` (the up neighbour's bottom halo row, a full storage row
+ * of (cols+2)*pitch(levels) doubles) and its last row into `halo_down` (the down
+ * neighbour's top halo row), column images included -- P2P stores over NVLink when the
+ * pointers are peer / IPC mappings (tsg_ipc_open).  NULL pointers skip that side. */
+int tsg_mpdata_step_rows_peer(tsg_grid *g, const double *pd, const double *vn, const double *wn,
+                              const double *rho, const double *signs, const double *dual,
+                              double *pd_out, double dt, double pivbz, int flux_op, int row_lo,
+                              int row_hi, double *halo_up, double *halo_down, tsg_stream s);
 /* Four-kernel step materialising flux (edges), fluz (vertices, levels+1) and divvd
  * (vertices) like run_naive (executors.py:213-245), halos refreshed after each stage. */
 int tsg_mpdata_step_unfused(const tsg_grid *g, const double *pd, const double *vn,
@@ -175,6 +184,22 @@ int tsg_make_permutation(int rows, int cols, int loc, int numbering, int64_t *fo
 int64_t tsg_permutation_work_elems(int rows, int cols, int loc);
 /* Orientation signs [n_vertices, 6] in canonical order (connectivity.py:184-194). */
 int tsg_edge_signs(int rows, int cols, double *out, tsg_stream s);
+
+/* ---- cross-GPU plumbing for the fused exchange (one process per GPU) ------------------ */
+/* Device memory outside any caching allocator (IPC handles need whole allocations). */
+int tsg_malloc(int64_t bytes, void **out);
+int tsg_free(void *ptr);
+/* CUDA IPC: export an allocation (64-byte handle) / map a peer's allocation. */
+int tsg_ipc_handle(void *ptr, unsigned char *handle64);
+int tsg_ipc_open(const unsigned char *handle64, void **out);
+int tsg_ipc_close(void *ptr);
+/* Step fence between neighbours: after a step, store `value` into both neighbours' flag
+ * words (system-scope release); before the next step's boundary rows, wait until this
+ * rank's two flag words reach `value` (spin with back-off; gives up after `timeout_ms` and
+ * reports TSG_ECUDA through the error word so a lost peer cannot hang the GPU). */
+int tsg_signal_peers(int64_t *flag_up, int64_t *flag_down, int64_t value, tsg_stream s);
+int tsg_wait_flags(const int64_t *my_flags, int64_t value, int timeout_ms, int *error_word,
+                   tsg_stream s);
 
 /* ---- diagnostics / synthetic inputs ----------------------------------------------- */
 /* sum_v sum_k pd[v,k] * dual[v] (mpdata.py:496-500), deterministic two-pass reduction;

@@ -34,6 +34,15 @@ SIGNATURES = {
     "tsg_mpdata_step": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _c_dbl, _c_dbl, _c_int, _p]),
     "tsg_mpdata_step_rows": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _c_dbl, _c_dbl, _c_int, _c_int,
                                       _c_int, _p]),
+    "tsg_mpdata_step_rows_peer": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _c_dbl, _c_dbl, _c_int,
+                                           _c_int, _c_int, _p, _p, _p]),
+    "tsg_malloc": (_c_int, [_c_i64, ctypes.POINTER(_p)]),
+    "tsg_free": (_c_int, [_p]),
+    "tsg_ipc_handle": (_c_int, [_p, ctypes.c_char_p]),
+    "tsg_ipc_open": (_c_int, [ctypes.c_char_p, ctypes.POINTER(_p)]),
+    "tsg_ipc_close": (_c_int, [_p]),
+    "tsg_signal_peers": (_c_int, [_p, _p, _c_i64, _p]),
+    "tsg_wait_flags": (_c_int, [_p, _c_i64, _c_int, _p, _p]),
     "tsg_mpdata_step_unfused": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _c_dbl,
                                          _c_dbl, _c_int, _p]),
     "tsg_transport_indirect": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _c_i64, _c_i64, _c_int,

@@ -126,6 +126,9 @@ struct FusedArgs {
     int rows, cols, K;
     int row_lo, row_hi;  // rows computed by this launch: [row_lo, row_hi)
     int flags;
+    // fused halo exchange: the ring neighbours' halo rows (peer / IPC-mapped memory) that
+    // receive this strip's first / last row; NULL = not exchanged by this kernel
+    double *halo_up, *halo_down;
     double dt, pivbz;
     int tiles_j, chunks;
     int64_t units;
@@ -211,6 +214,7 @@ __global__ void __launch_bounds__(TI *TJ * LV)
     bool vvalid = false;
     double sg0 = 0, sg1 = 0, sg2 = 0, sg3 = 0, sg4 = 0, sg5 = 0, dual = 1.0;
     double *out = nullptr;
+    double *peer = nullptr;        // neighbour's halo row element receiving this vertex
     int64_t d_row = 0, d_col = 0;  // offsets of the periodic halo images (0 = none)
 
     for (int n = 0; n < n_units; ++n) {
@@ -232,6 +236,9 @@ __global__ void __launch_bounds__(TI *TJ * LV)
                 out = a.pd_out + cell * pv;
                 d_row = 0;
                 d_col = 0;
+                peer = nullptr;
+                if (i == 0 && a.halo_up) peer = a.halo_up + (int64_t)(j + 1) * pv;
+                else if (i == a.rows - 1 && a.halo_down) peer = a.halo_down + (int64_t)(j + 1) * pv;
                 if (a.flags & TSG_PERIODIC_ROWS) {
                     if (i == 0) d_row = (int64_t)a.rows * rowstride;
                     else if (i == a.rows - 1) d_row = -(int64_t)a.rows * rowstride;
@@ -299,6 +306,10 @@ __global__ void __launch_bounds__(TI *TJ * LV)
                     if (d_row) o[d_row] = val;
                     if (d_col) o[d_col] = val;
                     if (d_row && d_col) o[d_row + d_col] = val;
+                }
+                if (peer) {  // fused halo exchange: store straight into the neighbour
+                    peer[k] = val;
+                    if (d_col) peer[k + d_col] = val;
                 }
             }
         }
@@ -430,7 +441,19 @@ extern "C" int tsg_mpdata_step_rows(tsg_grid *g, const double *pd, const double 
                                     const double *wn, const double *rho, const double *signs,
                                     const double *dual, double *pd_out, double dt, double pivbz,
                                     int flux_op, int row_lo, int row_hi, tsg_stream s) {
+    return tsg_mpdata_step_rows_peer(g, pd, vn, wn, rho, signs, dual, pd_out, dt, pivbz, flux_op,
+                                     row_lo, row_hi, nullptr, nullptr, s);
+}
+
+extern "C" int tsg_mpdata_step_rows_peer(tsg_grid *g, const double *pd, const double *vn,
+                                         const double *wn, const double *rho,
+                                         const double *signs, const double *dual, double *pd_out,
+                                         double dt, double pivbz, int flux_op, int row_lo,
+                                         int row_hi, double *halo_up, double *halo_down,
+                                         tsg_stream s) {
     if (!g) return fail(TSG_EVALUE, "grid is NULL");
+    if ((halo_up || halo_down) && (g->flags & TSG_PERIODIC_ROWS))
+        return fail(TSG_EVALUE, "peer halo rows need a row strip (no periodic rows)");
     if (row_lo < 0 || row_hi > g->rows || row_lo > row_hi)
         return fail(TSG_EVALUE, "row range [%d, %d) outside [0, %d)", row_lo, row_hi, g->rows);
     if (row_lo == row_hi) return TSG_OK;
@@ -481,6 +504,8 @@ extern "C" int tsg_mpdata_step_rows(tsg_grid *g, const double *pd, const double 
     a.cols = cols;
     a.row_lo = row_lo;
     a.row_hi = row_hi;
+    a.halo_up = halo_up;
+    a.halo_down = halo_down;
     a.K = K;
     a.flags = g->flags;
     a.dt = dt;

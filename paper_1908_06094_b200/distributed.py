@@ -63,11 +63,68 @@ def exchange_halo_rows(field: torch.Tensor, nrows: int, rank: int, world: int, g
     if world == 1:
         return []
     up, down = (rank - 1) % world, (rank + 1) % world
+    if field.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo moves host tensors only: stage the two rows through host memory
+        host = field[[0, 1, nrows, nrows + 1]].cpu()
+        reqs = exchange_halo_rows(host, 2, rank, world, group)
+        wait_all(reqs)
+        field[0].copy_(host[0])
+        field[nrows + 1].copy_(host[3])
+        return []
     ops = [dist.P2POp(dist.isend, field[nrows], down, group),   # last interior -> down's top halo
            dist.P2POp(dist.isend, field[1], up, group),         # first interior -> up's bottom halo
            dist.P2POp(dist.irecv, field[0], up, group),         # top halo <- up's last interior
            dist.P2POp(dist.irecv, field[nrows + 1], down, group)]  # bottom halo <- down's first
     return dist.batch_isend_irecv(ops)
+
+
+class RawBuffer:
+    """A whole cudaMalloc allocation (IPC-exportable) viewed as a torch tensor."""
+
+    def __init__(self, shape, dtype="<f8", ptr=None, owned=True):
+        import ctypes
+
+        import numpy as np
+
+        self.shape, self.dtype = tuple(shape), dtype
+        self.nbytes = int(np.prod(self.shape)) * np.dtype(dtype).itemsize
+        self.owned = owned
+        if ptr is None:
+            p = ctypes.c_void_p()
+            _lib.call("tsg_malloc", self.nbytes, ctypes.byref(p))
+            ptr = p.value
+        self.ptr = ptr
+        self.__cuda_array_interface__ = {"shape": self.shape, "typestr": dtype,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+        self.tensor = torch.as_tensor(self, device="cuda")
+
+    def ipc_handle(self) -> bytes:
+        import ctypes
+
+        buf = ctypes.create_string_buffer(64)
+        _lib.call("tsg_ipc_handle", ctypes.c_void_p(self.ptr), buf)
+        return buf.raw
+
+    @classmethod
+    def open(cls, handle: bytes) -> "RawBuffer":
+        import ctypes
+
+        p = ctypes.c_void_p()
+        _lib.call("tsg_ipc_open", handle, ctypes.byref(p))
+        obj = cls.__new__(cls)
+        obj.ptr, obj.owned, obj.shape = p.value, False, None
+        return obj
+
+    def __del__(self):
+        import ctypes
+
+        lib = _lib._lib
+        if lib is None or not getattr(self, "ptr", None):
+            return
+        if self.owned:
+            lib.tsg_free(ctypes.c_void_p(self.ptr))
+        else:
+            lib.tsg_ipc_close(ctypes.c_void_p(self.ptr))
 
 
 def wait_all(reqs) -> None:
@@ -84,7 +141,8 @@ class StripStepper:
     """
 
     def __init__(self, global_rows: int, cols: int, levels: int, rank: int, world: int,
-                 seed: int = 0, group=None, flux_op: str = "upwind", exchange=None):
+                 seed: int = 0, group=None, flux_op: str = "upwind", exchange=None,
+                 mode: str = "nccl", timeout_ms: int = 20000):
         self.strips = RowStrips(global_rows, world)
         self.rank, self.world, self.group = rank, world, group
         self.row0, self.nrows = self.strips.strip(rank)
@@ -93,7 +151,17 @@ class StripStepper:
         self.grid = DeviceGrid(self.nrows, cols, levels, flags, self.row0, global_rows)
         self.flux_code = {"upwind": 0, "centred": 1}[flux_op]
         g, K = self.grid, levels
-        self.pd, self.pd_out = g.empty(0, K), g.empty(0, K)
+        if mode not in ("nccl", "p2p"):
+            raise ValueError(f"exchange mode must be 'nccl' or 'p2p', got {mode!r}")
+        self.mode = mode if world > 1 else "nccl"
+        self.timeout_ms = timeout_ms
+        self.steps_done = 0
+        if self.mode == "p2p":
+            # the density buffers are whole cudaMalloc allocations so they can be IPC-exported
+            self._raw = [RawBuffer(g.field_shape(0, K)) for _ in range(2)]
+            self.pd, self.pd_out = (b.tensor for b in self._raw)
+        else:
+            self.pd, self.pd_out = g.empty(0, K), g.empty(0, K)
         self.vn, self.wn, self.rho = g.empty(2, K), g.empty(0, K + 1), g.empty(0, K)
         self.signs, self.dual = g.empty(0, 6), g.empty(0, 1)
         self.comm = torch.cuda.Stream()
@@ -101,6 +169,38 @@ class StripStepper:
         # exchange(field, nrows, rank, world, group) -> requests; replaceable for in-process use
         self.exchange = exchange or exchange_halo_rows
         self._fill_synthetic(seed)
+        if self.mode == "p2p":
+            self._setup_peers()
+
+    def _setup_peers(self) -> None:
+        """Exchange IPC handles with the ring neighbours and map their density buffers."""
+        import ctypes
+
+        self._flags = RawBuffer((2,), dtype="<i8")
+        self._err = RawBuffer((1,), dtype="<i4")
+        mine = (self._raw[0].ipc_handle(), self._raw[1].ipc_handle(), self._flags.ipc_handle(),
+                self.nrows)
+        every = [None] * self.world
+        dist.all_gather_object(every, mine, group=self.group)
+        self._peers = {}
+        for r in {self.strips.up(self.rank), self.strips.down(self.rank)}:
+            h0, h1, hf, nr = every[r]
+            bufs = [RawBuffer.open(h) for h in (h0, h1)]
+            self._peers[r] = dict(bufs=bufs, flags=RawBuffer.open(hf), nrows=nr)
+        self._rowstride = self.pd.stride(0) * 8  # bytes per storage row
+        self._parity = 0  # pd = raw[parity], pd_out = raw[1 - parity]
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+
+    def _peer_rows(self):
+        """(up neighbour's bottom halo row, down neighbour's top halo row) of their pd_out."""
+        import ctypes
+
+        up, down = self._peers[self.strips.up(self.rank)], self._peers[self.strips.down(self.rank)]
+        b = 1 - self._parity
+        hu = ctypes.c_void_p(up["bufs"][b].ptr + (up["nrows"] + 1) * self._rowstride)
+        hd = ctypes.c_void_p(down["bufs"][b].ptr)
+        return hu, hd
 
     def _fill_synthetic(self, seed: int) -> None:
         s = _lib.stream_handle()
@@ -139,6 +239,9 @@ class StripStepper:
         if self.world == 1:
             self._launch(0, self.nrows, dt, pivbz, main)
             return
+        if self.mode == "p2p":
+            self._step_p2p(dt, pivbz, main)
+            return
         # interior rows need no halo: overlap them with the previous exchange
         self._launch(1, self.nrows - 1, dt, pivbz, main)
         wait_all(self.pending)  # makes `main` wait for the halo rows of pd
@@ -151,8 +254,36 @@ class StripStepper:
         with torch.cuda.stream(self.comm):
             self.pending = self.exchange(self.pd_out, self.nrows, self.rank, self.world, self.group)
 
+    def _step_p2p(self, dt: float, pivbz: float, main) -> None:
+        """Fused exchange: the boundary rows' epilogue stores into the neighbours' halos."""
+        import ctypes
+
+        n, s = self.steps_done, _lib.stream_handle(main)
+        self._launch(1, self.nrows - 1, dt, pivbz, main)  # interior: no halo, no peers
+        # neighbours finished step n-1: my halo rows are complete and their pd_out is free
+        _lib.call("tsg_wait_flags", ctypes.c_void_p(self._flags.ptr), n, self.timeout_ms,
+                  ctypes.c_void_p(self._err.ptr), s)
+        hu, hd = self._peer_rows()
+        args = [self.grid.handle, _lib.ptr(self.pd), _lib.ptr(self.vn), _lib.ptr(self.wn),
+                _lib.ptr(self.rho), _lib.ptr(self.signs), _lib.ptr(self.dual), _lib.ptr(self.pd_out),
+                float(dt), float(pivbz), self.flux_code]
+        _lib.call("tsg_mpdata_step_rows_peer", *args, 0, 1, hu, None, s)
+        _lib.call("tsg_mpdata_step_rows_peer", *args, self.nrows - 1, self.nrows, None, hd, s)
+        up, down = self._peers[self.strips.up(self.rank)], self._peers[self.strips.down(self.rank)]
+        # I am my up neighbour's down neighbour (its flag word 1) and vice versa
+        _lib.call("tsg_signal_peers", ctypes.c_void_p(up["flags"].ptr + 8),
+                  ctypes.c_void_p(down["flags"].ptr), n + 1, s)
+
+    def check(self) -> None:
+        """Raise if a step fence timed out (a neighbour never arrived)."""
+        if self.mode == "p2p" and int(self._err.tensor.item()):
+            raise RuntimeError("fused halo exchange: a neighbour did not reach the step fence")
+
     def swap(self) -> None:
         self.pd, self.pd_out = self.pd_out, self.pd
+        self.steps_done += 1
+        if self.mode == "p2p":
+            self._parity = 1 - self._parity
 
     def finish(self) -> None:
         wait_all(self.pending)
