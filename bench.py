@@ -193,9 +193,12 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # TSG_SHARE_ONE_GPU=1: every rank on cuda:0 with gloo -- exercises the N>1 code path on
+    # a one-GPU box (not a performance configuration)
+    shared = os.environ.get("TSG_SHARE_ONE_GPU") == "1"
+    torch.cuda.set_device(0 if shared else local)
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if shared else "nccl")
     if args.variant:
         _lib.call("tsg_set_fused_variant", args.variant)
 
@@ -255,7 +258,7 @@ def run_ours(args):
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_s = sum(step_ms) / 1e3
     if world > 1:
-        t = torch.tensor([total_s], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_s], dtype=torch.float64, device="cpu" if shared else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_s = float(t.item())
     mean_step = total_s / args.steps
