@@ -360,3 +360,52 @@ def test_pipelined_host_fed_steps_match_oracle(cuda_ok):
     torch.cuda.synchronize()
     for o, w in zip(outs, want):
         assert np.array_equal(o.numpy(), w)
+
+
+def test_dump_tables_and_csv_loading(cuda_ok):
+    import io
+
+    spec = T.PatchSpec(3, 4, 2)
+    buf = io.StringIO()
+    T.dump_tables(spec, buf)
+    rows = buf.getvalue().strip().splitlines()
+    assert rows[0] == "from_loc,to_loc,element,slot,neighbor"
+    got = {}
+    for ln in rows[1:]:
+        f, t, e, s, nb = ln.split(",")
+        got.setdefault((f, t), {})[(int(e), int(s))] = int(nb)
+    for (f, t) in O.OFFSETS:
+        want = O.neighbor_table(3, 4, f, t)
+        assert all(got[(f, t)][(e, s)] == want[e, s] for e in range(want.shape[0]) for s in range(want.shape[1]))
+    field = T.make_storage(spec, L.EDGES, "vn")
+    T.load_field_csv(field, io.StringIO("element,level,value\n# comment\n0,0,1.5\n35,1,-2.25\n"))
+    flat = T.field_to_flat(field)
+    assert flat[0, 0] == 1.5 and flat[35, 1] == -2.25 and np.count_nonzero(flat) == 2
+    with pytest.raises(ValueError, match="out of range"):
+        T.load_field_csv(field, io.StringIO("36,0,1.0\n"))
+
+
+def test_time_computation_and_runstats(cuda_ok):
+    spec = T.PatchSpec(16, 12, 6)
+    geo, state = _case(spec, 4)
+    comp = T.build_mpdata(spec, state, geo, T.MpdataParams())
+    res = T.time_computation(comp, lambda c: T.run_gpu(c, download=False), reps=3)
+    assert res.updates == spec.rows * spec.cols * (6 * spec.levels + 1)
+    assert len(res.times) == 3 and res.median_seconds > 0
+    stats = T.run_gpu(comp)
+    assert stats.wall_times["ms0"] > 0 and stats.traffic()["algorithmic_bytes"] > 0
+    with pytest.raises(ValueError):
+        T.time_computation(comp, T.run_fused, reps=0)
+
+
+def test_device_resident_results_follow_the_staleness_contract(cuda_ok):
+    spec = T.PatchSpec(6, 7, 5)
+    geo, state = _case(spec, 2)
+    comp = T.build_mpdata(spec, state, geo, T.MpdataParams(dt=0.2, pivbz=0.8))
+    want = _oracle(spec, geo, state, T.MpdataParams(dt=0.2, pivbz=0.8))
+    T.run_gpu(comp, download=False)
+    with pytest.raises(T.StalenessError):
+        state.pd_out.array("primary")
+    assert np.array_equal(T.field_to_flat(state.pd_out), want["pd_out"])  # unpacked on device
+    T.sync(state.pd_out, "primary")
+    assert np.array_equal(T.field_to_flat(state.pd_out), want["pd_out"])
