@@ -42,7 +42,7 @@ __global__ void unpack_kernel(FieldIx F, int inner, PointDec D, const double *__
 }
 
 // element-line variants (one warp per element, lanes along the level run) for long runs
-__global__ void __launch_bounds__(256, 6) pack_lines_kernel(FieldIx F, int inner,
+__global__ void __launch_bounds__(256) pack_lines_kernel(FieldIx F, int inner,
                                                          const double *__restrict__ flat,
                                                          const int64_t *__restrict__ forward,
                                                          double *__restrict__ f, int flags) {
@@ -51,11 +51,15 @@ __global__ void __launch_bounds__(256, 6) pack_lines_kernel(FieldIx F, int inner
         const double *src = flat + (forward ? __ldg(forward + id) : id) * inner;
         double *o = f + F.at(i, c, j);
         const Img m = images(F, i, j, flags);
-        for (int k = threadIdx.x; k < inner; k += 32) put(o, m, k, src[k]);
+        if ((inner & 1) == 0) {  // level pairs: flat rows are 16-byte aligned too
+            for (int k = 2 * threadIdx.x; k < inner; k += 64) put2(o, m, k, ld2(src + k));
+        } else {
+            for (int k = threadIdx.x; k < inner; k += 32) put(o, m, k, src[k]);
+        }
     }
 }
 
-__global__ void __launch_bounds__(256, 6) unpack_lines_kernel(FieldIx F, int inner,
+__global__ void __launch_bounds__(256) unpack_lines_kernel(FieldIx F, int inner,
                                                            const double *__restrict__ f,
                                                            const int64_t *__restrict__ forward,
                                                            double *__restrict__ flat) {
@@ -63,7 +67,11 @@ __global__ void __launch_bounds__(256, 6) unpack_lines_kernel(FieldIx F, int inn
         const int64_t id = ((int64_t)i * F.colors + c) * F.cols + j;
         double *dst = flat + (forward ? __ldg(forward + id) : id) * inner;
         const double *src = f + F.at(i, c, j);
-        for (int k = threadIdx.x; k < inner; k += 32) dst[k] = src[k];
+        if ((inner & 1) == 0) {
+            for (int k = 2 * threadIdx.x; k < inner; k += 64) st2(dst + k, ld2(src + k));
+        } else {
+            for (int k = threadIdx.x; k < inner; k += 32) dst[k] = src[k];
+        }
     }
 }
 
@@ -399,8 +407,8 @@ extern "C" int tsg_pack(const tsg_grid *g, int loc, int inner, const double *fla
     if (!PointDec::fits(g->rows, g->cols, F.colors, inner)) return fail(TSG_EVALUE, "field too large");
     PointDec D(g->rows, g->cols, F.colors, inner);
     if (inner >= 16)
-        pack_lines_kernel<<<line_grid(g->cols, (int64_t)g->rows * F.colors, g->num_sms), line_block(), 0,
-                            (cudaStream_t)s>>>(F, inner, flat, forward, field, g->flags);
+        launch_lines(pack_lines_kernel, g->cols, (int64_t)g->rows * F.colors, g->num_sms,
+                     (cudaStream_t)s, F, inner, flat, forward, field, g->flags);
     else
         pack_kernel<<<grid_for(D.n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(F, inner, D, flat,
                                                                                  forward, field, g->flags);
@@ -417,8 +425,8 @@ extern "C" int tsg_unpack(const tsg_grid *g, int loc, int inner, const double *f
     if (!PointDec::fits(g->rows, g->cols, F.colors, inner)) return fail(TSG_EVALUE, "field too large");
     PointDec D(g->rows, g->cols, F.colors, inner);
     if (inner >= 16)
-        unpack_lines_kernel<<<line_grid(g->cols, (int64_t)g->rows * F.colors, g->num_sms), line_block(), 0,
-                              (cudaStream_t)s>>>(F, inner, field, forward, flat);
+        launch_lines(unpack_lines_kernel, g->cols, (int64_t)g->rows * F.colors, g->num_sms,
+                     (cudaStream_t)s, F, inner, field, forward, flat);
     else
         unpack_kernel<<<grid_for(D.n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(F, inner, D, field,
                                                                                    forward, flat);

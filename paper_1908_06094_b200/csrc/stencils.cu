@@ -12,7 +12,7 @@ namespace tsg {
 // -- structured reduce over any relation (stencil.py:404-408 with the sum fold) -------
 
 template <int REL, bool SCALE>
-__global__ void __launch_bounds__(256, 6) reduce_kernel(FieldIx Fs, FieldIx Fd, FieldIx Fsc, int nk,
+__global__ void __launch_bounds__(256) reduce_kernel(FieldIx Fs, FieldIx Fd, FieldIx Fsc, int nk,
                                                      const double *__restrict__ src,
                                                      const double *__restrict__ scale,
                                                      double *__restrict__ dst, int flags) {
@@ -27,12 +27,24 @@ __global__ void __launch_bounds__(256, 6) reduce_kernel(FieldIx Fs, FieldIx Fd, 
         const double sc = SCALE ? scale[Fsc.at(i, c, j)] : 1.0;
         double *out = dst + Fd.at(i, c, j);
         const Img m = images(Fd, i, j, flags);
-        for (int k = threadIdx.x; k < nk; k += 32) {
+        if (nk > 1) {  // level pairs, 16-byte accesses
+            for (int k = 2 * threadIdx.x; k < nk; k += 64) {
+                double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int s = 0; s < W; ++s) {
+                    const double2 v = ld2(nb[s] + k);
+                    acc.x = add(v.x, acc.x);
+                    acc.y = add(v.y, acc.y);
+                }
+                if (SCALE) acc = make_double2(mul(acc.x, sc), mul(acc.y, sc));
+                put2(out, m, k, acc);
+            }
+        } else if (threadIdx.x == 0) {
             double acc = 0.0;
 #pragma unroll
-            for (int s = 0; s < W; ++s) acc = add(nb[s][k], acc);
+            for (int s = 0; s < W; ++s) acc = add(nb[s][0], acc);
             if (SCALE) acc = mul(acc, sc);
-            put(out, m, k, acc);
+            put(out, m, 0, acc);
         }
     }
 }
@@ -40,7 +52,7 @@ __global__ void __launch_bounds__(256, 6) reduce_kernel(FieldIx Fs, FieldIx Fd, 
 // -- table-driven reduce over flat arrays (kernels.py:83-104, reference.py:137-157) -----
 
 template <int W>
-__global__ void __launch_bounds__(256, 6) reduce_indirect_kernel(const int64_t *__restrict__ table,
+__global__ void __launch_bounds__(256) reduce_indirect_kernel(const int64_t *__restrict__ table,
                                                               int64_t nrows, int width, int nlev,
                                                               const double *__restrict__ src,
                                                               const double *__restrict__ scale,
@@ -51,7 +63,21 @@ __global__ void __launch_bounds__(256, 6) reduce_indirect_kernel(const int64_t *
         const int64_t *row = table + r * wd;
         const double sc = scale ? scale[r] : 1.0;
         double *out = dst + r * nlev;
-        if (W > 0) {
+        if (W > 0 && (nlev & 1) == 0) {  // level pairs, 16-byte accesses
+            const double *nb[W > 0 ? W : 1];
+#pragma unroll
+            for (int s = 0; s < W; ++s) nb[s] = src + __ldg(row + s) * nlev;
+            for (int k = 2 * threadIdx.x; k < nlev; k += 64) {
+                double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int s = 0; s < W; ++s) {
+                    const double2 v = ld2(nb[s] + k);
+                    acc.x = add(v.x, acc.x);
+                    acc.y = add(v.y, acc.y);
+                }
+                st2(out + k, scale ? make_double2(mul(acc.x, sc), mul(acc.y, sc)) : acc);
+            }
+        } else if (W > 0) {
             const double *nb[W > 0 ? W : 1];
 #pragma unroll
             for (int s = 0; s < W; ++s) nb[s] = src + __ldg(row + s) * nlev;
@@ -74,7 +100,7 @@ __global__ void __launch_bounds__(256, 6) reduce_indirect_kernel(const int64_t *
 // -- cell divergence (mpdata.py:361-416, reference.py:119-134) --------------------------
 
 template <bool WEIGHTED>
-__global__ void __launch_bounds__(256, 6) cell_div_kernel(FieldIx Fvn, FieldIx Fl, FieldIx Fa,
+__global__ void __launch_bounds__(256) cell_div_kernel(FieldIx Fvn, FieldIx Fl, FieldIx Fa,
                                                        FieldIx Fw, FieldIx Fo, int nk,
                                                        const double *__restrict__ vn,
                                                        const double *__restrict__ length,
@@ -107,7 +133,7 @@ __global__ void __launch_bounds__(256, 6) cell_div_kernel(FieldIx Fvn, FieldIx F
 // -- unfused MPDATA (run_naive analogue, executors.py:213-245) --------------------------
 
 template <int OP>
-__global__ void __launch_bounds__(256, 6) flux_kernel(FieldIx Fp, FieldIx Fe, int K,
+__global__ void __launch_bounds__(256) flux_kernel(FieldIx Fp, FieldIx Fe, int K,
                                                    const double *__restrict__ pd,
                                                    const double *__restrict__ vn,
                                                    double *__restrict__ flux, int flags) {
@@ -122,7 +148,7 @@ __global__ void __launch_bounds__(256, 6) flux_kernel(FieldIx Fp, FieldIx Fe, in
     }
 }
 
-__global__ void __launch_bounds__(256, 6) fluz_kernel(FieldIx Fp, FieldIx Fw, int K, double pivbz,
+__global__ void __launch_bounds__(256) fluz_kernel(FieldIx Fp, FieldIx Fw, int K, double pivbz,
                                                    const double *__restrict__ pd,
                                                    const double *__restrict__ wn,
                                                    double *__restrict__ fluz, int flags) {
@@ -141,7 +167,7 @@ __global__ void __launch_bounds__(256, 6) fluz_kernel(FieldIx Fp, FieldIx Fw, in
     }
 }
 
-__global__ void __launch_bounds__(256, 6) div_kernel(FieldIx Fe, FieldIx Fw, FieldIx Fs, FieldIx Fd,
+__global__ void __launch_bounds__(256) div_kernel(FieldIx Fe, FieldIx Fw, FieldIx Fs, FieldIx Fd,
                                                   FieldIx Fv, int K, const double *__restrict__ flux,
                                                   const double *__restrict__ fluz,
                                                   const double *__restrict__ signs,
@@ -172,7 +198,7 @@ __global__ void __launch_bounds__(256, 6) div_kernel(FieldIx Fe, FieldIx Fw, Fie
     }
 }
 
-__global__ void __launch_bounds__(256, 6) advance_kernel(FieldIx Fv, int K, double dt,
+__global__ void __launch_bounds__(256) advance_kernel(FieldIx Fv, int K, double dt,
                                                       const double *__restrict__ pd,
                                                       const double *__restrict__ divvd,
                                                       const double *__restrict__ rho,
@@ -195,7 +221,7 @@ __global__ void __launch_bounds__(256, 6) advance_kernel(FieldIx Fv, int K, doub
          r += (int64_t)gridDim.x * kWarps)
 
 template <int OP>
-__global__ void __launch_bounds__(256, 6) iflux_kernel(const int64_t *__restrict__ e2v, int64_t ne,
+__global__ void __launch_bounds__(256) iflux_kernel(const int64_t *__restrict__ e2v, int64_t ne,
                                                     int K, const double *__restrict__ pd,
                                                     const double *__restrict__ vn,
                                                     double *__restrict__ flux) {
@@ -207,7 +233,7 @@ __global__ void __launch_bounds__(256, 6) iflux_kernel(const int64_t *__restrict
     }
 }
 
-__global__ void __launch_bounds__(256, 6) ifluz_kernel(int64_t nv, int K, double pivbz,
+__global__ void __launch_bounds__(256) ifluz_kernel(int64_t nv, int K, double pivbz,
                                                     const double *__restrict__ pd,
                                                     const double *__restrict__ wn,
                                                     double *__restrict__ fluz) {
@@ -224,7 +250,7 @@ __global__ void __launch_bounds__(256, 6) ifluz_kernel(int64_t nv, int K, double
     }
 }
 
-__global__ void __launch_bounds__(256, 6) idiv_advance_kernel(
+__global__ void __launch_bounds__(256) idiv_advance_kernel(
     const int64_t *__restrict__ v2e, int64_t nv, int K, double dt, const double *__restrict__ signs,
     const double *__restrict__ dual, const double *__restrict__ flux,
     const double *__restrict__ fluz, const double *__restrict__ pd, const double *__restrict__ rho,
@@ -276,15 +302,17 @@ extern "C" int tsg_neighbor_reduce(const tsg_grid *g, int from_loc, int to_loc, 
     FieldIx Fs(g->rows, g->cols, colors_of(to_loc), inner);
     FieldIx Fd(g->rows, g->cols, colors_of(from_loc), inner);
     FieldIx Fsc(g->rows, g->cols, colors_of(from_loc), 1);
-    const dim3 grid = line_grid(g->cols, (int64_t)g->rows * Fd.colors, g->num_sms), block = line_block();
     cudaStream_t st = (cudaStream_t)s;
     const int rel = from_loc * 3 + to_loc;
-#define TSG_REDUCE_CASE(R)                                                                          \
-    case R:                                                                                        \
-        if (scale)                                                                                 \
-            reduce_kernel<R, true><<<grid, block, 0, st>>>(Fs, Fd, Fsc, inner, src, scale, dst, g->flags); \
-        else                                                                                       \
-            reduce_kernel<R, false><<<grid, block, 0, st>>>(Fs, Fd, Fsc, inner, src, scale, dst, g->flags); \
+    const int64_t lines = (int64_t)g->rows * Fd.colors;
+#define TSG_REDUCE_CASE(R)                                                                        \
+    case R:                                                                                      \
+        if (scale)                                                                               \
+            launch_lines(reduce_kernel<R, true>, g->cols, lines, g->num_sms, st, Fs, Fd, Fsc,     \
+                         inner, src, scale, dst, g->flags);                                      \
+        else                                                                                     \
+            launch_lines(reduce_kernel<R, false>, g->cols, lines, g->num_sms, st, Fs, Fd, Fsc,    \
+                         inner, src, scale, dst, g->flags);                                      \
         break;
     switch (rel) {
         TSG_REDUCE_CASE(0) TSG_REDUCE_CASE(1) TSG_REDUCE_CASE(2) TSG_REDUCE_CASE(3)
@@ -303,14 +331,14 @@ extern "C" int tsg_neighbor_reduce_indirect(const int64_t *table, int64_t nrows,
     if (nrows < 0 || width < 1 || nlev < 1)
         return fail(TSG_EVALUE, "bad table shape (%lld, %d) / levels %d", (long long)nrows, width, nlev);
     if (nrows == 0) return TSG_OK;
-    const int nb = flat_blocks(nrows, sm_count());
+    const int sms = sm_count();
     cudaStream_t st = (cudaStream_t)s;
     switch (width) {
-        case 2: reduce_indirect_kernel<2><<<nb, line_block(), 0, st>>>(table, nrows, width, nlev, src, scale, dst); break;
-        case 3: reduce_indirect_kernel<3><<<nb, line_block(), 0, st>>>(table, nrows, width, nlev, src, scale, dst); break;
-        case 4: reduce_indirect_kernel<4><<<nb, line_block(), 0, st>>>(table, nrows, width, nlev, src, scale, dst); break;
-        case 6: reduce_indirect_kernel<6><<<nb, line_block(), 0, st>>>(table, nrows, width, nlev, src, scale, dst); break;
-        default: reduce_indirect_kernel<0><<<nb, line_block(), 0, st>>>(table, nrows, width, nlev, src, scale, dst);
+        case 2: launch_rows(reduce_indirect_kernel<2>, nrows, sms, st, table, nrows, width, nlev, src, scale, dst); break;
+        case 3: launch_rows(reduce_indirect_kernel<3>, nrows, sms, st, table, nrows, width, nlev, src, scale, dst); break;
+        case 4: launch_rows(reduce_indirect_kernel<4>, nrows, sms, st, table, nrows, width, nlev, src, scale, dst); break;
+        case 6: launch_rows(reduce_indirect_kernel<6>, nrows, sms, st, table, nrows, width, nlev, src, scale, dst); break;
+        default: launch_rows(reduce_indirect_kernel<0>, nrows, sms, st, table, nrows, width, nlev, src, scale, dst);
     }
     TSG_CHECK_LAUNCH();
     return TSG_OK;
@@ -325,13 +353,12 @@ extern "C" int tsg_cell_divergence(const tsg_grid *g, int weighted, const double
     int K = g->levels;
     FieldIx Fvn(g->rows, g->cols, 3, K), Fl(g->rows, g->cols, 3, 1), Fa(g->rows, g->cols, 2, 1),
         Fw(g->rows, g->cols, 2, 3), Fo(g->rows, g->cols, 2, K);
-    const dim3 grid = line_grid(g->cols, 2LL * g->rows, g->num_sms);
     if (weighted)
-        cell_div_kernel<true><<<grid, line_block(), 0, (cudaStream_t)s>>>(
-            Fvn, Fl, Fa, Fw, Fo, K, vn, length, area, weights, out, g->flags);
+        launch_lines(cell_div_kernel<true>, g->cols, 2LL * g->rows, g->num_sms, (cudaStream_t)s, Fvn,
+                     Fl, Fa, Fw, Fo, K, vn, length, area, weights, out, g->flags);
     else
-        cell_div_kernel<false><<<grid, line_block(), 0, (cudaStream_t)s>>>(
-            Fvn, Fl, Fa, Fw, Fo, K, vn, length, area, weights, out, g->flags);
+        launch_lines(cell_div_kernel<false>, g->cols, 2LL * g->rows, g->num_sms, (cudaStream_t)s, Fvn,
+                     Fl, Fa, Fw, Fo, K, vn, length, area, weights, out, g->flags);
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }
@@ -356,14 +383,16 @@ extern "C" int tsg_mpdata_step_unfused(const tsg_grid *g, const double *pd, cons
     cudaStream_t st = (cudaStream_t)s;
     FieldIx Fv(g->rows, g->cols, 1, K), Fe(g->rows, g->cols, 3, K), Fw(g->rows, g->cols, 1, K + 1),
         Fs(g->rows, g->cols, 1, 6), Fd(g->rows, g->cols, 1, 1);
-    const dim3 gE = line_grid(g->cols, 3LL * g->rows, g->num_sms), gV = line_grid(g->cols, g->rows, g->num_sms), b = line_block();
+    const int C = g->cols, sms = g->num_sms;
+    const int64_t lE = 3LL * g->rows, lV = g->rows;
     if (flux_op == TSG_UPWIND)
-        flux_kernel<TSG_UPWIND><<<gE, b, 0, st>>>(Fv, Fe, K, pd, vn, flux, g->flags);
+        launch_lines(flux_kernel<TSG_UPWIND>, C, lE, sms, st, Fv, Fe, K, pd, vn, flux, g->flags);
     else
-        flux_kernel<TSG_CENTRED><<<gE, b, 0, st>>>(Fv, Fe, K, pd, vn, flux, g->flags);
-    fluz_kernel<<<gV, b, 0, st>>>(Fv, Fw, K, pivbz, pd, wn, fluz, g->flags);
-    div_kernel<<<gV, b, 0, st>>>(Fe, Fw, Fs, Fd, Fv, K, flux, fluz, signs, dual, divvd, g->flags);
-    advance_kernel<<<gV, b, 0, st>>>(Fv, K, dt, pd, divvd, rho, pd_out, g->flags);
+        launch_lines(flux_kernel<TSG_CENTRED>, C, lE, sms, st, Fv, Fe, K, pd, vn, flux, g->flags);
+    launch_lines(fluz_kernel, C, lV, sms, st, Fv, Fw, K, pivbz, pd, wn, fluz, g->flags);
+    launch_lines(div_kernel, C, lV, sms, st, Fe, Fw, Fs, Fd, Fv, K, flux, fluz, signs, dual, divvd,
+                 g->flags);
+    launch_lines(advance_kernel, C, lV, sms, st, Fv, K, dt, pd, divvd, rho, pd_out, g->flags);
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }
@@ -380,14 +409,13 @@ extern "C" int tsg_transport_indirect(const int64_t *e2v, const int64_t *v2e, co
     if (nv < 1 || ne < 1) return fail(TSG_EVALUE, "empty mesh (nv=%lld, ne=%lld)", (long long)nv, (long long)ne);
     cudaStream_t st = (cudaStream_t)s;
     const int sms = sm_count();
-    const dim3 b = line_block();
     if (flux_op == TSG_UPWIND)
-        iflux_kernel<TSG_UPWIND><<<flat_blocks(ne, sms), b, 0, st>>>(e2v, ne, nlev, pd, vn, flux);
+        launch_rows(iflux_kernel<TSG_UPWIND>, ne, sms, st, e2v, ne, nlev, pd, vn, flux);
     else
-        iflux_kernel<TSG_CENTRED><<<flat_blocks(ne, sms), b, 0, st>>>(e2v, ne, nlev, pd, vn, flux);
-    ifluz_kernel<<<flat_blocks(nv, sms), b, 0, st>>>(nv, nlev, pivbz, pd, wn, fluz);
-    idiv_advance_kernel<<<flat_blocks(nv, sms), b, 0, st>>>(v2e, nv, nlev, dt, signs, dual, flux, fluz,
-                                                           pd, rho, div, pd_out);
+        launch_rows(iflux_kernel<TSG_CENTRED>, ne, sms, st, e2v, ne, nlev, pd, vn, flux);
+    launch_rows(ifluz_kernel, nv, sms, st, nv, nlev, pivbz, pd, wn, fluz);
+    launch_rows(idiv_advance_kernel, nv, sms, st, v2e, nv, nlev, dt, signs, dual, flux, fluz, pd, rho,
+                div, pd_out);
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }

@@ -6,6 +6,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #include "tsg.h"
 
 struct tsg_grid {
@@ -136,27 +139,51 @@ __device__ __forceinline__ void store_img(double *f, const FieldIx &F, int i, in
 // table rows are resolved once per element and reused for every level.
 constexpr int kWarps = 8;
 
-inline dim3 line_grid(int cols, int64_t lines, int num_sms = 148) {
-    // enough blocks for 8 resident blocks (2048 threads) per SM; each block then walks
-    // several (row, colour) lines, so short kernels are not dominated by block launches
-    const int64_t gx = (cols + kWarps - 1) / kWarps;
-    int64_t gy = ((int64_t)num_sms * 8 + gx - 1) / gx;
-    if (gy > lines) gy = lines;
-    if (gy > 65535) gy = 65535;
-    return dim3((unsigned)gx, (unsigned)(gy < 1 ? 1 : gy));
+// resident 256-thread blocks per SM of a kernel (cached occupancy query)
+inline int resident_blocks(const void *kernel) {
+    static std::mutex mu;
+    static std::unordered_map<const void *, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(kernel);
+    if (it != cache.end()) return it->second;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, 32 * kWarps, 0) != cudaSuccess || n < 1)
+        n = 1;
+    cache[kernel] = n;
+    return n;
+}
+
+// exactly one wave of resident blocks; blocks then walk their share of the work items
+inline dim3 one_wave(const void *kernel, int64_t items, int num_sms) {
+    int64_t g = (int64_t)num_sms * resident_blocks(kernel);
+    if (g > items) g = items;
+    return dim3((unsigned)(g < 1 ? 1 : g));
 }
 inline dim3 line_block() { return dim3(32, kWarps); }
 
-inline int flat_blocks(int64_t rows, int num_sms) {
-    int64_t b = (rows + kWarps - 1) / kWarps, cap = (int64_t)num_sms * 32;
-    return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+// launch an element-line kernel over `lines` (row, colour) lines of `cols` elements
+template <typename... Params, typename... Args>
+inline void launch_lines(void (*kernel)(Params...), int cols, int64_t lines, int num_sms,
+                         cudaStream_t st, Args... args) {
+    const int64_t items = lines * ((cols + kWarps - 1) / kWarps);
+    kernel<<<one_wave((const void *)kernel, items, num_sms), line_block(), 0, st>>>(args...);
 }
 
-#define TSG_LINES(F, i, c, j)                                                              \
-    const int j = blockIdx.x * kWarps + threadIdx.y;                                       \
-    if (j >= (F).cols) return;                                                             \
-    for (int line_ = blockIdx.y; line_ < (F).rows * (F).colors; line_ += gridDim.y)        \
-        for (int i = line_ / (F).colors, c = line_ - i * (F).colors, once_ = 1; once_; once_ = 0)
+// launch a flat-row kernel (one warp per table row) over `rows` rows
+template <typename... Params, typename... Args>
+inline void launch_rows(void (*kernel)(Params...), int64_t rows, int num_sms, cudaStream_t st,
+                        Args... args) {
+    kernel<<<one_wave((const void *)kernel, (rows + kWarps - 1) / kWarps, num_sms), line_block(), 0,
+             st>>>(args...);
+}
+
+#define TSG_LINES(F, i, c, j)                                                                  \
+    for (int item_ = blockIdx.x, ngrp_ = ((F).cols + kWarps - 1) / kWarps,                       \
+             nitem_ = (F).rows * (F).colors * ngrp_;                                             \
+         item_ < nitem_; item_ += gridDim.x)                                                     \
+        for (int line_ = item_ / ngrp_, j = (item_ - line_ * ngrp_) * kWarps + threadIdx.y,      \
+                 i = line_ / (F).colors, c = line_ - i * (F).colors, once_ = 1;                  \
+             once_ && j < (F).cols; once_ = 0)
 
 // offsets of the periodic halo images of element (i, j) (0 = none)
 struct Img {
@@ -180,6 +207,19 @@ __device__ __forceinline__ void put(double *o, const Img &m, int k, double v) {
         if (m.dr) o[m.dr + k] = v;
         if (m.dc) o[m.dc + k] = v;
         if (m.dr && m.dc) o[m.dr + m.dc + k] = v;
+    }
+}
+
+// 16-byte level pairs: every structured field has an even pitch, so (k, k+1) with k even
+// is aligned; the partner of the last odd level is padding, which may be written.
+__device__ __forceinline__ double2 ld2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
+__device__ __forceinline__ void st2(double *p, double2 v) { *reinterpret_cast<double2 *>(p) = v; }
+__device__ __forceinline__ void put2(double *o, const Img &m, int k, double2 v) {
+    st2(o + k, v);
+    if (m.dr | m.dc) {
+        if (m.dr) st2(o + m.dr + k, v);
+        if (m.dc) st2(o + m.dc + k, v);
+        if (m.dr && m.dc) st2(o + m.dr + m.dc + k, v);
     }
 }
 
