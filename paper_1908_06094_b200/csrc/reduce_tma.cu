@@ -1,0 +1,193 @@
+// TMA-staged structured neighbour reduce: the paper's Table-1 "direct access" kernel and
+// every one of the nine relations (stencil.py:401-408 with the sum fold; kernels.py:27-59).
+//
+// Same pipeline as the fused MPDATA kernel: a persistent grid walks (TI x TJ tile) x
+// (KC-level chunk) units; one TMA box [TI+2][colours][TJ+2][KC] of the source field (the
+// tile plus its one-ring halo, all target colours) lands in a STAGES-deep shared-memory
+// ring per unit; one thread per (tile position, level) folds every from-colour's
+// neighbours from shared memory in canonical slot order and stores the result (and its
+// periodic halo images) coalesced.  Offsets are compile-time constants of the relation.
+#include "tsg_offsets.cuh"
+#include "tsg_tma.cuh"
+
+namespace tsg {
+
+constexpr int kRedTI = 4, kRedTJ = 16, kRedKC = 16, kRedStages = 3;
+
+template <int CT>
+struct RedCfg {
+    static constexpr int kThreads = kRedTI * kRedTJ * 16;
+    static constexpr int kBoxBytes = (kRedTI + 2) * CT * (kRedTJ + 2) * kRedKC * 8;
+    static constexpr int kStageBytes = (kBoxBytes + 127) / 128 * 128;
+    static constexpr int kSmemBytes = kRedStages * kStageBytes + 128;
+};
+
+struct RedArgs {
+    double *dst;
+    const double *scale;
+    int rows, cols, nk, flags;
+    int tiles_j, chunks;
+    int64_t units;
+};
+
+template <int REL, bool SCALE>
+__global__ void __launch_bounds__(kRedTI *kRedTJ * 16)
+    reduce_tma_kernel(const __grid_constant__ CUtensorMap tm_src, const RedArgs a) {
+    constexpr int CF = loc_colors(REL / 3), CT = loc_colors(REL % 3), W = rel_width(REL);
+    constexpr int TI = kRedTI, TJ = kRedTJ, KC = kRedKC, STAGES = kRedStages;
+    using C = RedCfg<CT>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * C::kStageBytes);
+
+    const int tid = threadIdx.x, kl = tid & 15, v = tid >> 4;
+    const int li = v / TJ, lj = v % TJ;
+    // source box [TI+2][CT][TJ+2][KC], origin (i0-1, colour 0, j0-1, k0)
+    constexpr int sJ = KC, sC = (TJ + 2) * KC, sI = CT * (TJ + 2) * KC;
+    const int oS = (li + 1) * sI + (lj + 1) * sJ + kl;
+
+    const int u_begin = (int)(a.units * blockIdx.x / gridDim.x);
+    const int u_end = (int)(a.units * (blockIdx.x + 1) / gridDim.x);
+    const int n_units = u_end - u_begin;
+    if (tid == 0) {
+        prefetch_tmap(&tm_src);
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    int p_chunk = u_begin % a.chunks, p_tile = u_begin / a.chunks;
+    int p_ti = p_tile / a.tiles_j, p_tj = p_tile % a.tiles_j;
+    auto issue_next = [&](int stage) {
+        uint64_t *bar = &bars[stage];
+        mbar_expect_tx(bar, C::kBoxBytes);
+        tma_load_4d(smem + stage * C::kStageBytes, &tm_src, bar, p_chunk * KC, p_tj * TJ, 0, p_ti * TI);
+        if (++p_chunk == a.chunks) {
+            p_chunk = 0;
+            if (++p_tj == a.tiles_j) {
+                p_tj = 0;
+                ++p_ti;
+            }
+        }
+    };
+    if (tid == 0)
+        for (int s = 0; s < STAGES - 1 && s < n_units; ++s) issue_next(s);
+
+    int chunk = u_begin % a.chunks, tile = u_begin / a.chunks;
+    int ti = tile / a.tiles_j, tj = tile % a.tiles_j;
+    const int64_t pv = pitch_of(a.nk);
+    const FieldIx Fd(a.rows, a.cols, CF, a.nk), Fsc(a.rows, a.cols, CF, 1);
+    bool valid = false;
+    double *out[CF];
+    double sc[CF];
+    int64_t dr = 0, dc = 0;
+
+    for (int n = 0; n < n_units; ++n) {
+        const int stage = n % STAGES;
+        if (tid == 0 && n + STAGES - 1 < n_units) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_next((n + STAGES - 1) % STAGES);
+        }
+        if (n == 0 || chunk == 0) {
+            const int i = ti * TI + li, j = tj * TJ + lj;
+            valid = i < a.rows && j < a.cols;
+            if (valid) {
+#pragma unroll
+                for (int c = 0; c < CF; ++c) {
+                    out[c] = a.dst + Fd.at(i, c, j);
+                    sc[c] = SCALE ? __ldg(a.scale + Fsc.at(i, c, j)) : 1.0;
+                }
+                dr = 0;
+                dc = 0;
+                if (a.flags & TSG_PERIODIC_ROWS) {
+                    if (i == 0) dr = (int64_t)a.rows * Fd.rowstr;
+                    else if (i == a.rows - 1) dr = -(int64_t)a.rows * Fd.rowstr;
+                }
+                if (a.flags & TSG_PERIODIC_COLS) {
+                    if (j == 0) dc = (int64_t)a.cols * pv;
+                    else if (j == a.cols - 1) dc = -(int64_t)a.cols * pv;
+                }
+            }
+        }
+        mbar_wait(&bars[stage], (uint32_t)((n / STAGES) & 1));
+        const int k = chunk * KC + kl;
+        if (valid && k < a.nk) {
+            const double *S = reinterpret_cast<const double *>(smem + stage * C::kStageBytes) + oS;
+#pragma unroll
+            for (int c = 0; c < CF; ++c) {
+                double acc = 0.0;
+#pragma unroll
+                for (int s = 0; s < W; ++s)
+                    acc = add(S[rel_off(REL, c, s, 0) * sI + rel_off(REL, c, s, 1) * sC +
+                                rel_off(REL, c, s, 2) * sJ],
+                              acc);
+                if (SCALE) acc = mul(acc, sc[c]);
+                double *o = out[c] + k;
+                o[0] = acc;
+                if (dr | dc) {
+                    if (dr) o[dr] = acc;
+                    if (dc) o[dc] = acc;
+                    if (dr && dc) o[dr + dc] = acc;
+                }
+            }
+        }
+        if (++chunk == a.chunks) {
+            chunk = 0;
+            if (++tj == a.tiles_j) {
+                tj = 0;
+                ++ti;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <int REL, bool SCALE>
+static int launch_reduce_tma(const tsg_grid *g, int inner, const double *src, const double *scale,
+                             double *dst, cudaStream_t st) {
+    constexpr int CT = loc_colors(REL % 3);
+    using C = RedCfg<CT>;
+    if (int rc = get_encode()) return rc;
+    const cuuint64_t p = (cuuint64_t)pitch_of(inner), W = (cuuint64_t)g->cols + 2, H = (cuuint64_t)g->rows + 2;
+    cuuint64_t dims[4] = {p, W, (cuuint64_t)CT, H};
+    cuuint64_t str[3] = {p * 8, W * p * 8, CT * W * p * 8};
+    cuuint32_t box[4] = {kRedKC, kRedTJ + 2, (cuuint32_t)CT, kRedTI + 2};
+    CUtensorMap m;
+    if (int rc = make_map(&m, src, 4, dims, str, box)) return rc;
+    RedArgs a;
+    a.dst = dst;
+    a.scale = scale;
+    a.rows = g->rows;
+    a.cols = g->cols;
+    a.nk = inner;
+    a.flags = g->flags;
+    a.tiles_j = (g->cols + kRedTJ - 1) / kRedTJ;
+    a.chunks = (inner + kRedKC - 1) / kRedKC;
+    a.units = (int64_t)((g->rows + kRedTI - 1) / kRedTI) * a.tiles_j * a.chunks;
+    if (a.units >= (1LL << 31)) return fail(TSG_EVALUE, "field too large for one reduce launch");
+    void *fn = (void *)reduce_tma_kernel<REL, SCALE>;
+    TSG_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
+    int per_sm = 0;
+    TSG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, C::kThreads, C::kSmemBytes));
+    int64_t grid = (int64_t)g->num_sms * (per_sm < 1 ? 1 : per_sm);
+    if (grid > a.units) grid = a.units;
+    void *args[] = {&m, &a};
+    TSG_CHECK_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(C::kThreads), args, C::kSmemBytes, st));
+    return TSG_OK;
+}
+
+// dispatch over the nine relations; returns TSG_OK or an error
+int reduce_tma(const tsg_grid *g, int rel, int inner, const double *src, const double *scale,
+               double *dst, cudaStream_t st) {
+#define TSG_RT_CASE(R)                                                                  \
+    case R:                                                                            \
+        return scale ? launch_reduce_tma<R, true>(g, inner, src, scale, dst, st)       \
+                     : launch_reduce_tma<R, false>(g, inner, src, scale, dst, st);
+    switch (rel) {
+        TSG_RT_CASE(0) TSG_RT_CASE(1) TSG_RT_CASE(2) TSG_RT_CASE(3) TSG_RT_CASE(4)
+        TSG_RT_CASE(5) TSG_RT_CASE(6) TSG_RT_CASE(7) TSG_RT_CASE(8)
+    }
+#undef TSG_RT_CASE
+    return fail(TSG_EVALUE, "bad relation %d", rel);
+}
+
+}  // namespace tsg

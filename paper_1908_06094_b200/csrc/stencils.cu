@@ -9,6 +9,9 @@
 
 namespace tsg {
 
+int reduce_tma(const tsg_grid *g, int rel, int inner, const double *src, const double *scale,
+               double *dst, cudaStream_t st);
+
 // -- structured reduce over any relation (stencil.py:404-408 with the sum fold) -------
 
 template <int REL, bool SCALE>
@@ -304,6 +307,9 @@ extern "C" int tsg_neighbor_reduce(const tsg_grid *g, int from_loc, int to_loc, 
     FieldIx Fsc(g->rows, g->cols, colors_of(from_loc), 1);
     cudaStream_t st = (cudaStream_t)s;
     const int rel = from_loc * 3 + to_loc;
+    // long level runs: the TMA-staged tile kernel (reduce_tma.cu); short ones: element lines
+    if (inner >= 16 && (reinterpret_cast<uintptr_t>(src) % 16) == 0)
+        return reduce_tma(g, rel, inner, src, scale, dst, st);
     const int64_t lines = (int64_t)g->rows * Fd.colors;
 #define TSG_REDUCE_CASE(R)                                                                        \
     case R:                                                                                      \

@@ -33,6 +33,27 @@ static __constant__ int8_t c_offsets[9][3][6][3] = {
      {{0, 1, 0}, {1, 0, 0}, {0, 0, -1}, {0, 1, -1}}},
 };
 
+// the same table as a compile-time constant (for kernels templated on the relation; the
+// calls fold to immediates when rel, c, s are constants)
+__host__ __device__ constexpr int rel_off(int rel, int c, int s, int q) {
+    constexpr int8_t t[9][3][6][3] = {
+    {{{0, 0, 1}, {1, 0, 1}, {1, 0, 0}, {0, 0, -1}, {-1, 0, -1}, {-1, 0, 0}}},
+    {{{0, 0, 0}, {0, 1, 0}, {0, 0, -1}, {-1, 1, -1}, {-1, 0, -1}, {-1, 1, 0}}},
+    {{{0, 0, 0}, {0, 1, 0}, {0, 2, 0}, {0, 0, -1}, {-1, 1, -1}, {-1, 2, 0}}},
+    {{{0, 0, 0}, {0, 0, 1}, {1, 0, 1}}, {{0, 0, 0}, {1, 0, 0}, {1, 0, 1}}},
+    {{{0, 1, 0}, {-1, 1, 0}, {0, 1, 1}}, {{0, 0, 0}, {0, 0, -1}, {1, 0, 0}}},
+    {{{0, 0, 0}, {0, 1, 0}, {0, 2, 1}}, {{0, 2, 0}, {0, 1, 0}, {1, 0, 0}}},
+    {{{0, 0, 0}, {0, 0, 1}}, {{0, 0, 0}, {1, 0, 1}}, {{0, 0, 0}, {1, 0, 0}}},
+    {{{0, 0, 0}, {-1, 1, 0}}, {{0, 0, 0}, {0, 1, 0}}, {{0, 1, 0}, {0, 0, -1}}},
+    {{{0, 1, 0}, {0, 2, 1}, {-1, 2, 0}, {-1, 1, 0}},
+     {{0, 0, 0}, {0, 2, 1}, {0, 2, 0}, {1, 0, 0}},
+     {{0, 1, 0}, {1, 0, 0}, {0, 0, -1}, {0, 1, -1}}},
+};
+    return t[rel][c][s][q];
+}
+__host__ __device__ constexpr int rel_width(int rel) { return rel < 3 ? 6 : (rel < 6 ? 3 : (rel == 8 ? 4 : 2)); }
+__host__ __device__ constexpr int loc_colors(int loc) { return loc == 0 ? 1 : (loc == 1 ? 2 : 3); }
+
 inline int host_rel_width(int from_loc, int to_loc) {
     static const int w[9] = {6, 6, 6, 3, 3, 3, 2, 2, 4};
     return w[from_loc * 3 + to_loc];
