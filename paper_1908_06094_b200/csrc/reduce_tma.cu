@@ -25,12 +25,16 @@ struct RedCfg {
 struct RedArgs {
     double *dst;
     const double *scale;
+    const double *length, *area, *weights;  // cell divergence (MODE 1 / 2)
     int rows, cols, nk, flags;
     int tiles_j, chunks;
     int64_t units;
 };
 
-template <int REL, bool SCALE>
+// MODE 0: sum fold (times scale[from] if SCALE); MODE 1: cell divergence
+// sum vn*length / area; MODE 2: weighted cell divergence sum vn*weights[c, n]
+// (mpdata.py:361-376; reference.py:119-134)
+template <int REL, bool SCALE, int MODE = 0>
 __global__ void __launch_bounds__(kRedTI *kRedTJ * 16)
     reduce_tma_kernel(const __grid_constant__ CUtensorMap tm_src, const RedArgs a) {
     constexpr int CF = loc_colors(REL / 3), CT = loc_colors(REL % 3), W = rel_width(REL);
@@ -79,6 +83,7 @@ __global__ void __launch_bounds__(kRedTI *kRedTJ * 16)
     bool valid = false;
     double *out[CF];
     double sc[CF];
+    double w[MODE ? CF : 1][MODE ? W : 1];  // per-element edge weights (cell divergence)
     int64_t dr = 0, dc = 0;
 
     for (int n = 0; n < n_units; ++n) {
@@ -95,6 +100,18 @@ __global__ void __launch_bounds__(kRedTI *kRedTJ * 16)
                 for (int c = 0; c < CF; ++c) {
                     out[c] = a.dst + Fd.at(i, c, j);
                     sc[c] = SCALE ? __ldg(a.scale + Fsc.at(i, c, j)) : 1.0;
+                    if constexpr (MODE == 1) {
+                        const FieldIx Fl(a.rows, a.cols, 3, 1);
+                        sc[c] = __ldg(a.area + Fsc.at(i, c, j));
+#pragma unroll
+                        for (int q = 0; q < W; ++q)
+                            w[c][q] = __ldg(a.length + Fl.at(i + rel_off(REL, c, q, 0), rel_off(REL, c, q, 1),
+                                                             j + rel_off(REL, c, q, 2)));
+                    } else if constexpr (MODE == 2) {
+                        const FieldIx Fw(a.rows, a.cols, CF, 3);
+#pragma unroll
+                        for (int q = 0; q < W; ++q) w[c][q] = __ldg(a.weights + Fw.at(i, c, j) + q);
+                    }
                 }
                 dr = 0;
                 dc = 0;
@@ -116,11 +133,13 @@ __global__ void __launch_bounds__(kRedTI *kRedTJ * 16)
             for (int c = 0; c < CF; ++c) {
                 double acc = 0.0;
 #pragma unroll
-                for (int s = 0; s < W; ++s)
-                    acc = add(S[rel_off(REL, c, s, 0) * sI + rel_off(REL, c, s, 1) * sC +
-                                rel_off(REL, c, s, 2) * sJ],
-                              acc);
+                for (int s = 0; s < W; ++s) {
+                    const double x = S[rel_off(REL, c, s, 0) * sI + rel_off(REL, c, s, 1) * sC +
+                                       rel_off(REL, c, s, 2) * sJ];
+                    acc = MODE ? add(mul(x, w[c][s]), acc) : add(x, acc);
+                }
                 if (SCALE) acc = mul(acc, sc[c]);
+                if (MODE == 1) acc = dvd(acc, sc[c]);
                 double *o = out[c] + k;
                 o[0] = acc;
                 if (dr | dc) {
@@ -141,9 +160,10 @@ __global__ void __launch_bounds__(kRedTI *kRedTJ * 16)
     }
 }
 
-template <int REL, bool SCALE>
+template <int REL, bool SCALE, int MODE = 0>
 static int launch_reduce_tma(const tsg_grid *g, int inner, const double *src, const double *scale,
-                             double *dst, cudaStream_t st) {
+                             double *dst, cudaStream_t st, const double *length = nullptr,
+                             const double *area = nullptr, const double *weights = nullptr) {
     constexpr int CT = loc_colors(REL % 3);
     using C = RedCfg<CT>;
     if (int rc = get_encode()) return rc;
@@ -156,6 +176,9 @@ static int launch_reduce_tma(const tsg_grid *g, int inner, const double *src, co
     RedArgs a;
     a.dst = dst;
     a.scale = scale;
+    a.length = length;
+    a.area = area;
+    a.weights = weights;
     a.rows = g->rows;
     a.cols = g->cols;
     a.nk = inner;
@@ -164,7 +187,7 @@ static int launch_reduce_tma(const tsg_grid *g, int inner, const double *src, co
     a.chunks = (inner + kRedKC - 1) / kRedKC;
     a.units = (int64_t)((g->rows + kRedTI - 1) / kRedTI) * a.tiles_j * a.chunks;
     if (a.units >= (1LL << 31)) return fail(TSG_EVALUE, "field too large for one reduce launch");
-    void *fn = (void *)reduce_tma_kernel<REL, SCALE>;
+    void *fn = (void *)reduce_tma_kernel<REL, SCALE, MODE>;
     TSG_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
     int per_sm = 0;
     TSG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, C::kThreads, C::kSmemBytes));
@@ -188,6 +211,15 @@ int reduce_tma(const tsg_grid *g, int rel, int inner, const double *src, const d
     }
 #undef TSG_RT_CASE
     return fail(TSG_EVALUE, "bad relation %d", rel);
+}
+
+int cell_divergence_tma(const tsg_grid *g, int weighted, const double *vn, const double *length,
+                        const double *area, const double *weights, double *out, cudaStream_t st) {
+    constexpr int REL = TSG_CELLS * 3 + TSG_EDGES;
+    return weighted ? launch_reduce_tma<REL, false, 2>(g, g->levels, vn, nullptr, out, st, nullptr,
+                                                      nullptr, weights)
+                    : launch_reduce_tma<REL, false, 1>(g, g->levels, vn, nullptr, out, st, length, area,
+                                                      nullptr);
 }
 
 }  // namespace tsg

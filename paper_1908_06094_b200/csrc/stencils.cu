@@ -11,6 +11,8 @@ namespace tsg {
 
 int reduce_tma(const tsg_grid *g, int rel, int inner, const double *src, const double *scale,
                double *dst, cudaStream_t st);
+int cell_divergence_tma(const tsg_grid *g, int weighted, const double *vn, const double *length,
+                        const double *area, const double *weights, double *out, cudaStream_t st);
 
 // -- structured reduce over any relation (stencil.py:404-408 with the sum fold) -------
 
@@ -359,6 +361,8 @@ extern "C" int tsg_cell_divergence(const tsg_grid *g, int weighted, const double
     int K = g->levels;
     FieldIx Fvn(g->rows, g->cols, 3, K), Fl(g->rows, g->cols, 3, 1), Fa(g->rows, g->cols, 2, 1),
         Fw(g->rows, g->cols, 2, 3), Fo(g->rows, g->cols, 2, K);
+    if (K >= 16 && (reinterpret_cast<uintptr_t>(vn) % 16) == 0)
+        return cell_divergence_tma(g, weighted, vn, length, area, weights, out, (cudaStream_t)s);
     if (weighted)
         launch_lines(cell_div_kernel<true>, g->cols, 2LL * g->rows, g->num_sms, (cudaStream_t)s, Fvn,
                      Fl, Fa, Fw, Fo, K, vn, length, area, weights, out, g->flags);

@@ -409,3 +409,39 @@ def test_device_resident_results_follow_the_staleness_contract(cuda_ok):
     assert np.array_equal(T.field_to_flat(state.pd_out), want["pd_out"])  # unpacked on device
     T.sync(state.pd_out, "primary")
     assert np.array_equal(T.field_to_flat(state.pd_out), want["pd_out"])
+
+
+@pytest.mark.parametrize("shape", [(13, 21, 20), (6, 37, 33)])
+def test_tma_reduce_and_cell_divergence_paths(cuda_ok, shape):
+    """Long level runs take the TMA-staged kernels (reduce_tma.cu): all nine relations,
+    the scaled Table-1 kernel and both cell divergences against the oracle, bitwise."""
+    r, c, lev = shape
+    spec = T.PatchSpec(r, c, lev)
+    rng = np.random.default_rng(lev)
+    for (f, t) in T.OFFSET_TABLES:
+        src = T.make_storage(spec, t, "a")
+        dst = T.make_storage(spec, f, "b")
+        a = rng.random((T.element_count(spec, t), lev))
+        T.flat_to_field(a, src)
+        T.run_gpu(T.build_reduce(spec, f, t, src, dst))
+        want = O.neighbor_sum(O.neighbor_table(r, c, f.value, t.value), a)
+        assert np.array_equal(T.field_to_flat(dst), want), (f, t)
+    fields = T.make_kernel_fields(spec)
+    a = rng.random((2 * r * c, lev))
+    fac = 0.5 + rng.random((2 * r * c, 1))
+    T.flat_to_field(a, fields["a"])
+    T.flat_to_field(fac, fields["fac"])
+    T.run_gpu(T.build_kernel(spec, fields, True))
+    want = O.neighbor_sum_scaled(O.neighbor_table(r, c, "cells", "cells"), a, fac)
+    assert np.array_equal(T.field_to_flat(fields["b"]), want)
+    geo, state = _case(spec, 3)
+    c2e = O.neighbor_table(r, c, "cells", "edges")
+    vn = T.field_to_flat(state.vn)
+    length = T.field_to_flat(geo.edge_length)[:, 0]
+    area = T.field_to_flat(geo.cell_area)[:, 0]
+    weights = geo.weights.core()[:, :, :, 0, :].reshape(-1, 3)
+    for weighted, want in ((False, O.cell_divergence(c2e, vn, length, area)),
+                           (True, O.weighted_divergence(c2e, vn, weights))):
+        out = T.make_storage(spec, L.CELLS, "div_out")
+        T.run_gpu(T.build_divergence(spec, state, geo, weighted=weighted, out=out))
+        assert np.array_equal(T.field_to_flat(out), want), weighted
