@@ -10,9 +10,11 @@ Status codes map onto the reference's exception types (include/tsg.h).
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().with_name("libtsg.so")
+# TSG_LIBRARY overrides the in-tree build (A/B timing of two builds of the same ABI)
+LIB_PATH = Path(os.environ.get("TSG_LIBRARY") or Path(__file__).resolve().with_name("libtsg.so"))
 
 _c_int, _c_i64, _c_dbl, _c_u64 = ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_uint64
 _p = ctypes.c_void_p
@@ -77,6 +79,8 @@ def lib() -> ctypes.CDLL:
                 "or `make -C paper_1908_06094_b200/csrc` (this package has no CPU fallback)")
         handle = ctypes.CDLL(str(LIB_PATH))
         for name, (res, args) in SIGNATURES.items():
+            if "TSG_LIBRARY" in os.environ and not hasattr(handle, name):
+                continue  # an older build under A/B timing
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args

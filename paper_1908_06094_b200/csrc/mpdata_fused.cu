@@ -75,7 +75,9 @@ struct FusedArgs {
     int64_t units;
 };
 
-template <int TI, int TJ, int KC, int STAGES, int LV, int OP>
+// PEER: the launch stores its strip's boundary rows into the ring neighbours' halo rows
+// (a separate instantiation so the single-GPU kernel carries none of that epilogue)
+template <int TI, int TJ, int KC, int STAGES, int LV, int OP, bool PEER = false>
 __global__ void __launch_bounds__(TI *TJ * LV)
     mpdata_fused_kernel(const __grid_constant__ CUtensorMap tm_pd,
                         const __grid_constant__ CUtensorMap tm_vn,
@@ -177,9 +179,11 @@ __global__ void __launch_bounds__(TI *TJ * LV)
                 out = a.pd_out + cell * pv;
                 d_row = 0;
                 d_col = 0;
-                peer = nullptr;
-                if (i == 0 && a.halo_up) peer = a.halo_up + (int64_t)(j + 1) * pv;
-                else if (i == a.rows - 1 && a.halo_down) peer = a.halo_down + (int64_t)(j + 1) * pv;
+                if constexpr (PEER) {
+                    peer = nullptr;
+                    if (i == 0 && a.halo_up) peer = a.halo_up + (int64_t)(j + 1) * pv;
+                    else if (i == a.rows - 1 && a.halo_down) peer = a.halo_down + (int64_t)(j + 1) * pv;
+                }
                 if (a.flags & TSG_PERIODIC_ROWS) {
                     if (i == 0) d_row = (int64_t)a.rows * rowstride;
                     else if (i == a.rows - 1) d_row = -(int64_t)a.rows * rowstride;
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(TI *TJ * LV)
                     if (d_col) o[d_col] = val;
                     if (d_row && d_col) o[d_row + d_col] = val;
                 }
-                if (peer) {  // fused halo exchange: store straight into the neighbour
+                if (PEER && peer) {  // fused halo exchange: store straight into the neighbour
                     peer[k] = val;
                     if (d_col) peer[k + d_col] = val;
                 }
@@ -270,7 +274,8 @@ __global__ void __launch_bounds__(TI *TJ * LV)
 struct Variant {
     int ti, tj, kc, stages;
     int threads, smem;
-    void *fn[4];  // upwind, centred, data-movement probe, compute probe
+    void *fn[4];    // upwind, centred, data-movement probe, compute probe
+    void *peer[2];  // upwind, centred with the fused halo-row stores
 };
 
 template <int TI, int TJ, int KC, int STAGES, int LV = 16>
@@ -287,6 +292,8 @@ static Variant make_variant() {
     v.fn[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, TSG_CENTRED>;
     v.fn[2] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, kProbeOp>;
     v.fn[3] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, kComputeProbe>;
+    v.peer[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, TSG_UPWIND, true>;
+    v.peer[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, TSG_CENTRED, true>;
     return v;
 }
 
@@ -428,7 +435,11 @@ extern "C" int tsg_mpdata_step_rows_peer(tsg_grid *g, const double *pd, const do
     a.units = (int64_t)tiles_i * a.tiles_j * a.chunks;
     if (a.units >= (1LL << 31)) return fail(TSG_EVALUE, "patch too large for one fused launch");
 
-    void *fn = v.fn[flux_op == kProbeOp ? 2 : (flux_op == kComputeProbe ? 3 : flux_op)];
+    const bool peer = halo_up || halo_down;
+    if (peer && (flux_op == kProbeOp || flux_op == kComputeProbe))
+        return fail(TSG_EVALUE, "the probes do not exchange halo rows");
+    void *fn = peer ? v.peer[flux_op]
+                    : v.fn[flux_op == kProbeOp ? 2 : (flux_op == kComputeProbe ? 3 : flux_op)];
     TSG_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
     int per_sm = 0;
     TSG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, v.threads, v.smem));

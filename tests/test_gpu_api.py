@@ -265,6 +265,21 @@ def test_nan_and_signed_zero_semantics(cuda_ok):
         assert np.array_equal(np.signbit(un[k]), np.signbit(want[k])), k
 
 
+def test_extreme_dual_volumes(cuda_ok):
+    """Tiny, huge, subnormal, zero and negative dual volumes through the fused kernel."""
+    from tests.gpu_helpers import fused_step
+
+    r, c, lev = 9, 11, 20
+    inp = O.transport_inputs(r, c, lev, 3, "random", "random", "random")
+    d = inp["dual"].reshape(-1)
+    for v, x in enumerate([1e-300, 1e300, 5e-324, 0.0, -2.5, 2.0 ** -1022, 1.7e308, np.inf, 3.0]):
+        d[7 * v + 1] = x
+    with np.errstate(all="ignore"):
+        want = O.step_inputs(r, c, inp, 0.2, 0.8)["pd_out"]
+    got = fused_step(r, c, lev, inp, 0.2, 0.8)
+    assert np.array_equal(got, want, equal_nan=True)
+
+
 def test_every_fused_variant_is_bitwise_identical(cuda_ok):
     from paper_1908_06094_b200 import _lib
     from tests.gpu_helpers import fused_step
