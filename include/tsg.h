@@ -123,6 +123,14 @@ int tsg_mpdata_step_rows_peer(tsg_grid *g, const double *pd, const double *vn, c
                               const double *rho, const double *signs, const double *dual,
                               double *pd_out, double dt, double pivbz, int flux_op, int row_lo,
                               int row_hi, double *halo_up, double *halo_down, tsg_stream s);
+/* The reference's time loop (bench.py:398-403: step, copy pd_out -> pd_in, repeat) as a
+ * device ping-pong: step t reads pd_a and writes pd_b when t is even, the reverse when
+ * odd, so after nsteps the newest density is in pd_b (nsteps odd) or pd_a (even) and the
+ * other buffer holds the state before the last step.  vn / wn / rho / signs / dual are
+ * fixed over the loop, as in the reference; the tensor maps are encoded once. */
+int tsg_mpdata_run(tsg_grid *g, double *pd_a, double *pd_b, const double *vn, const double *wn,
+                   const double *rho, const double *signs, const double *dual, double dt,
+                   double pivbz, int flux_op, int nsteps, tsg_stream s);
 /* Four-kernel step materialising flux (edges), fluz (vertices, levels+1) and divvd
  * (vertices) like run_naive (executors.py:213-245), halos refreshed after each stage. */
 int tsg_mpdata_step_unfused(const tsg_grid *g, const double *pd, const double *vn,

@@ -52,6 +52,7 @@ from .executors import (
     halo_update,
     run_fused,
     run_gpu,
+    run_time_loop,
     run_naive,
     time_computation,
 )

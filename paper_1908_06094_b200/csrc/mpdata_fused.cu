@@ -364,18 +364,33 @@ extern "C" int tsg_mpdata_step_rows(tsg_grid *g, const double *pd, const double 
                                      row_lo, row_hi, nullptr, nullptr, s);
 }
 
-extern "C" int tsg_mpdata_step_rows_peer(tsg_grid *g, const double *pd, const double *vn,
-                                         const double *wn, const double *rho,
-                                         const double *signs, const double *dual, double *pd_out,
-                                         double dt, double pivbz, int flux_op, int row_lo,
-                                         int row_hi, double *halo_up, double *halo_down,
-                                         tsg_stream s) {
+// One prepared fused launch: tensor maps of the read-only inputs, the kernel arguments and
+// the grid, so a time loop encodes its maps once (tsg_mpdata_run).
+struct FusedLaunch {
+    CUtensorMap m_pd, m_vn, m_wn, m_rho;
+    FusedArgs a;
+    void *fn;
+    int grid, threads, smem;
+};
+
+static int encode_pd(const Variant &v, const tsg_grid *g, const double *pd, CUtensorMap *m) {
+    const cuuint64_t pv = (cuuint64_t)pitch_of(g->levels);
+    const cuuint64_t W = (cuuint64_t)g->cols + 2, H = (cuuint64_t)g->rows + 2;
+    cuuint64_t dims[3] = {pv, W, H};
+    cuuint64_t str[2] = {pv * 8, W * pv * 8};
+    cuuint32_t box[3] = {(cuuint32_t)v.kc + 4, (cuuint32_t)v.tj + 2, (cuuint32_t)v.ti + 2};
+    return make_map(m, pd, 3, dims, str, box);
+}
+
+static int prepare(tsg_grid *g, const double *pd, const double *vn, const double *wn,
+                   const double *rho, const double *signs, const double *dual, double *pd_out,
+                   double dt, double pivbz, int flux_op, int row_lo, int row_hi, double *halo_up,
+                   double *halo_down, FusedLaunch *L) {
     if (!g) return fail(TSG_EVALUE, "grid is NULL");
     if ((halo_up || halo_down) && (g->flags & TSG_PERIODIC_ROWS))
         return fail(TSG_EVALUE, "peer halo rows need a row strip (no periodic rows)");
     if (row_lo < 0 || row_hi > g->rows || row_lo > row_hi)
         return fail(TSG_EVALUE, "row range [%d, %d) outside [0, %d)", row_lo, row_hi, g->rows);
-    if (row_lo == row_hi) return TSG_OK;
     const int K = g->levels;
     if (K < 2) return fail(TSG_EVALUE, "the transport step needs at least 2 levels, got %d", K);
     if (flux_op != TSG_UPWIND && flux_op != TSG_CENTRED && flux_op != kProbeOp &&
@@ -384,6 +399,10 @@ extern "C" int tsg_mpdata_step_rows_peer(tsg_grid *g, const double *pd, const do
     if (!pd || !vn || !wn || !rho || !signs || !dual || !pd_out)
         return fail(TSG_EVALUE, "tsg_mpdata_step: NULL array");
     if (pd_out == pd) return fail(TSG_EVALUE, "pd_out must not alias pd (double-buffer the density)");
+    if (row_lo == row_hi) {  // nothing to compute: a valid no-op
+        L->a.units = 0;
+        return TSG_OK;
+    }
     if (int rc = get_encode()) return rc;
 
     int n = 0;
@@ -393,29 +412,27 @@ extern "C" int tsg_mpdata_step_rows_peer(tsg_grid *g, const double *pd, const do
     const int rows = g->rows, cols = g->cols;
     const cuuint64_t pv = (cuuint64_t)pitch_of(K), pw = (cuuint64_t)pitch_of(K + 1);
     const cuuint64_t W = (cuuint64_t)cols + 2, H = (cuuint64_t)rows + 2;
-    CUtensorMap m_pd, m_vn, m_wn, m_rho;
+    if (int rc = encode_pd(v, g, pd, &L->m_pd)) return rc;
     {
         cuuint64_t dims[3] = {pv, W, H};
         cuuint64_t str[2] = {pv * 8, W * pv * 8};
-        cuuint32_t box[3] = {(cuuint32_t)v.kc + 4, (cuuint32_t)v.tj + 2, (cuuint32_t)v.ti + 2};
-        if (int rc = make_map(&m_pd, pd, 3, dims, str, box)) return rc;
         cuuint32_t boxr[3] = {(cuuint32_t)v.kc, (cuuint32_t)v.tj, (cuuint32_t)v.ti};
-        if (int rc = make_map(&m_rho, rho, 3, dims, str, boxr)) return rc;
+        if (int rc = make_map(&L->m_rho, rho, 3, dims, str, boxr)) return rc;
     }
     {
         cuuint64_t dims[4] = {pv, W, 3, H};
         cuuint64_t str[3] = {pv * 8, W * pv * 8, 3 * W * pv * 8};
         cuuint32_t box[4] = {(cuuint32_t)v.kc, (cuuint32_t)v.tj + 1, 3, (cuuint32_t)v.ti + 1};
-        if (int rc = make_map(&m_vn, vn, 4, dims, str, box)) return rc;
+        if (int rc = make_map(&L->m_vn, vn, 4, dims, str, box)) return rc;
     }
     {
         cuuint64_t dims[3] = {pw, W, H};
         cuuint64_t str[2] = {pw * 8, W * pw * 8};
         cuuint32_t box[3] = {(cuuint32_t)v.kc + 2, (cuuint32_t)v.tj, (cuuint32_t)v.ti};
-        if (int rc = make_map(&m_wn, wn, 3, dims, str, box)) return rc;
+        if (int rc = make_map(&L->m_wn, wn, 3, dims, str, box)) return rc;
     }
 
-    FusedArgs a;
+    FusedArgs &a = L->a;
     a.signs = signs;
     a.dual = dual;
     a.pd_out = pd_out;
@@ -438,17 +455,61 @@ extern "C" int tsg_mpdata_step_rows_peer(tsg_grid *g, const double *pd, const do
     const bool peer = halo_up || halo_down;
     if (peer && (flux_op == kProbeOp || flux_op == kComputeProbe))
         return fail(TSG_EVALUE, "the probes do not exchange halo rows");
-    void *fn = peer ? v.peer[flux_op]
-                    : v.fn[flux_op == kProbeOp ? 2 : (flux_op == kComputeProbe ? 3 : flux_op)];
-    TSG_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
+    L->fn = peer ? v.peer[flux_op]
+                 : v.fn[flux_op == kProbeOp ? 2 : (flux_op == kComputeProbe ? 3 : flux_op)];
+    TSG_CHECK_CUDA(cudaFuncSetAttribute(L->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
     int per_sm = 0;
-    TSG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, v.threads, v.smem));
+    TSG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L->fn, v.threads, v.smem));
     if (per_sm < 1) return fail(TSG_ECUDA, "fused variant %d does not fit on an SM", g_variant);
     int64_t grid = (int64_t)g->num_sms * per_sm;
     if (grid > a.units) grid = a.units;
+    L->grid = (int)grid;
+    L->threads = v.threads;
+    L->smem = v.smem;
+    return TSG_OK;
+}
 
-    void *args[] = {&m_pd, &m_vn, &m_wn, &m_rho, &a};
-    TSG_CHECK_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(v.threads), args, v.smem,
+static int launch(FusedLaunch *L, tsg_stream s) {
+    if (L->a.units == 0) return TSG_OK;
+    void *args[] = {&L->m_pd, &L->m_vn, &L->m_wn, &L->m_rho, &L->a};
+    TSG_CHECK_CUDA(cudaLaunchKernel(L->fn, dim3((unsigned)L->grid), dim3(L->threads), args, L->smem,
                                     (cudaStream_t)s));
+    return TSG_OK;
+}
+
+extern "C" int tsg_mpdata_step_rows_peer(tsg_grid *g, const double *pd, const double *vn,
+                                         const double *wn, const double *rho,
+                                         const double *signs, const double *dual, double *pd_out,
+                                         double dt, double pivbz, int flux_op, int row_lo,
+                                         int row_hi, double *halo_up, double *halo_down,
+                                         tsg_stream s) {
+    FusedLaunch L;
+    if (int rc = prepare(g, pd, vn, wn, rho, signs, dual, pd_out, dt, pivbz, flux_op, row_lo,
+                         row_hi, halo_up, halo_down, &L))
+        return rc;
+    return launch(&L, s);
+}
+
+extern "C" int tsg_mpdata_run(tsg_grid *g, double *pd_a, double *pd_b, const double *vn,
+                              const double *wn, const double *rho, const double *signs,
+                              const double *dual, double dt, double pivbz, int flux_op, int nsteps,
+                              tsg_stream s) {
+    if (!g) return fail(TSG_EVALUE, "grid is NULL");
+    if (nsteps < 0) return fail(TSG_EVALUE, "nsteps must be >= 0, got %d", nsteps);
+    if (flux_op == kProbeOp || flux_op == kComputeProbe)
+        return fail(TSG_EVALUE, "flux operator must be one of ['centred', 'upwind'], got %d", flux_op);
+    if (nsteps == 0) return TSG_OK;
+    FusedLaunch fwd, bwd;  // a -> b and b -> a
+    if (int rc = prepare(g, pd_a, vn, wn, rho, signs, dual, pd_b, dt, pivbz, flux_op, 0, g->rows,
+                         nullptr, nullptr, &fwd))
+        return rc;
+    bwd = fwd;
+    bwd.a.pd_out = pd_a;
+    {
+        int n = 0;
+        if (int rc = encode_pd(variants(&n)[g_variant - 1], g, pd_b, &bwd.m_pd)) return rc;
+    }
+    for (int t = 0; t < nsteps; ++t)
+        if (int rc = launch(t % 2 == 0 ? &fwd : &bwd, s)) return rc;
     return TSG_OK;
 }

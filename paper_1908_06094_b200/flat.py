@@ -188,6 +188,21 @@ class StructuredStepper:
         """Time loop: the new density becomes the next step's input (no copy)."""
         self.pd, self.pd_out = self.pd_out, self.pd
 
+    def run(self, steps, dt, pivbz, flux_op="upwind", stream=None):
+        """``steps`` fused steps with fixed vn / wn / rho (bench.py:398-403), ping-ponging
+        the two density buffers on the device (tsg_mpdata_run).  Afterwards ``pd_out``
+        holds the newest density and ``pd`` the state before the last step, exactly as
+        after ``steps`` calls of step(); swap()."""
+        steps = int(steps)
+        if steps < 0:
+            raise ValueError(f"steps must be >= 0, got {steps}")
+        _lib.call("tsg_mpdata_run", self.grid.handle, _lib.ptr(self.pd), _lib.ptr(self.pd_out),
+                  _lib.ptr(self.vn), _lib.ptr(self.wn), _lib.ptr(self.rho), _lib.ptr(self.signs),
+                  _lib.ptr(self.dual), float(dt), float(pivbz), _FLUX_CODE[flux_op], steps,
+                  _lib.stream_handle(stream))
+        if steps and steps % 2 == 0:
+            self.swap()  # the newest density landed in the input buffer
+
     def download(self, out=None, stream=None):
         """Structured pd_out -> flat (numbering of perm_v) -> host ``out`` (pinned) or numpy."""
         _lib.call("tsg_unpack", self.grid.handle, 0, self.spec.levels, _lib.ptr(self.pd_out),

@@ -67,6 +67,41 @@ def test_field_api_naive_and_fused_match_oracle(cuda_ok, shape, seed):
     assert np.array_equal(arr[0], arr[spec.rows]) and np.array_equal(arr[:, :, -1], arr[:, :, 1])
 
 
+@pytest.mark.parametrize("steps", [1, 2, 3, 4])
+@pytest.mark.parametrize("fused", [True, False])
+def test_time_loop_matches_reference_loop(cuda_ok, steps, fused):
+    """run_time_loop == the reference's loop (bench.py:398-403): after it pd_out is the
+    final density and pd_in the state before the last step; both fields' halos stay
+    periodic images; intermediates (unfused) are the last step's."""
+    spec = T.PatchSpec(9, 14, 11)
+    params = T.MpdataParams(dt=0.2, pivbz=0.6)
+    geo, state = _case(spec, 11)
+    comp = T.build_mpdata(spec, state, geo, params)
+    r, c = spec.rows, spec.cols
+    e2v, v2e = O.neighbor_table(r, c, "edges", "vertices"), O.neighbor_table(r, c, "vertices", "edges")
+    dual = T.field_to_flat(geo.dual_volumes)[:, 0]
+    pd, vn, wn, rho = (T.field_to_flat(f) for f in (state.pd_in, state.vn, state.wn, state.rho))
+    prev = pd
+    for _ in range(steps):
+        prev, out = pd, O.transport_step(e2v, v2e, O.edge_signs(r, c), dual, pd, vn, wn, rho,
+                                         params.dt, params.pivbz)
+        pd = out["pd_out"]
+    stats = T.run_time_loop(comp, steps, fused=fused)
+    assert stats.total_updates == steps * r * c * (6 * spec.levels + 1)
+    assert np.array_equal(T.field_to_flat(state.pd_out), pd)
+    assert np.array_equal(T.field_to_flat(state.pd_in), prev)
+    if not fused:
+        assert np.array_equal(T.field_to_flat(state.divvd), out["div"])
+    for f in (state.pd_in, state.pd_out):
+        arr = f.array()
+        assert np.array_equal(arr[0], arr[r]) and np.array_equal(arr[:, :, -1], arr[:, :, 1])
+    # the swapped device buffers stay consistent for a following single step
+    T.run_fused(comp)
+    want = O.transport_step(e2v, v2e, O.edge_signs(r, c), dual, T.field_to_flat(state.pd_in), vn, wn, rho,
+                            params.dt, params.pivbz)["pd_out"]
+    assert np.array_equal(T.field_to_flat(state.pd_out), want)
+
+
 def test_level_inner_layout_and_wide_halo(cuda_ok):
     spec = T.PatchSpec(6, 5, 4, halo=2)
     lay = T.LayoutSpec(("extra", "row", "color", "column", "level"), 8)

@@ -114,3 +114,11 @@ def test_multistep_time_loop_matches_reference_hash(cuda_ok, golden_hashes):
         st.swap()
     st.swap()
     assert sha(st.download()) == e["outputs"]["pd_out"]
+    # the same loop as one device ping-pong (tsg_mpdata_run), odd and even counts
+    for split in ((e["steps"],), (3, e["steps"] - 3)):
+        st = stepper_for(44, 72, 10, inp)
+        for n in split:
+            st.run(n, e["dt"], e["pivbz"])
+            st.swap()
+        st.swap()
+        assert sha(st.download()) == e["outputs"]["pd_out"], split
