@@ -20,12 +20,15 @@
 //       rho [TI][TJ][KC]
 //    One elected thread issues the TMA for unit n+STAGES-1 while all threads compute
 //    unit n; __syncthreads() at the end of a unit releases its stage.
-//  * Compute: one thread per (vertex, level), 16 threads per vertex (a half-warp reads a
-//    contiguous 128-byte level run: conflict-free).  Each thread recomputes the six
-//    incident edge fluxes straight from smem (every edge flux is computed by both of its
-//    endpoints -- bitwise identical, no smem round trip, no extra barrier), the two
-//    interface fluxes, the divergence and the update, and stores pd_out (plus periodic
-//    halo images) straight to HBM, coalesced.
+//  * Compute (default variant 15): a thread owns an adjacent level pair (k, k+1) of one
+//    vertex, 8 threads per vertex, 512 threads per CTA.  A quarter-warp reads one vertex's
+//    contiguous 128-byte level run with 16-byte loads (conflict-free).  Each thread
+//    recomputes the six incident edge fluxes of both levels straight from smem (every edge
+//    flux is computed by both of its endpoints -- bitwise identical, no smem round trip, no
+//    extra barrier), the three interface fluxes k, k+1, k+2 (k+1 shared by the pair), the
+//    divergences and the updates, and stores the pd_out pair (plus periodic halo images)
+//    straight to HBM with one 16-byte store.  The LP = 1 variants (1-14) run one thread
+//    per (vertex, level) instead.
 //  * No tensor cores: fp64 stencil, ~0.5 flop/byte, the HBM roofline bounds it.
 #include "tsg_tma.cuh"
 
@@ -33,7 +36,7 @@ namespace tsg {
 
 // ---- tile geometry --------------------------------------------------------------------
 
-template <int TI, int TJ, int KC, int STAGES, int LV>
+template <int TI, int TJ, int KC, int STAGES, int LV, int LP = 1>
 struct FusedCfg {
     static constexpr int kThreads = TI * TJ * LV;                  // LV lanes per vertex
     static constexpr int kLevelsPerThread = (KC + LV - 1) / LV;  // last pass may be partial
@@ -50,7 +53,8 @@ struct FusedCfg {
     static constexpr uint32_t kTxBytes = kPdBytes + kVnBytes + kWnBytes + kRhoBytes;
     static constexpr int kSmemBytes = STAGES * kStageBytes + 128;  // + barriers
     static_assert(KC % 16 == 0, "KC must be a multiple of 16");
-    static_assert(LV == 16 || LV == 32, "a half-warp or a warp per vertex");
+    static_assert((LP == 1 && (LV == 16 || LV == 32)) || (LP == 2 && LV * 2 == KC),
+                  "a half-warp or a warp per vertex, or level pairs covering the chunk");
     static_assert(((KC + 2) * 8) % 16 == 0 && (KC * 8) % 16 == 0, "TMA inner box must be 16B multiple");
     static_assert(TI + 2 <= 256 && TJ + 2 <= 256 && KC + 4 <= 256, "TMA box <= 256");
 };
@@ -75,15 +79,18 @@ struct FusedArgs {
     int64_t units;
 };
 
+// LP: levels per thread.  LP = 1: thread per (vertex, level), LV lanes per vertex.
+// LP = 2: a thread owns the adjacent level pair (k, k+1): 16-byte shared loads and stores,
+// the shared interface flux k+1 computed once, half the per-unit overhead per point.
 // PEER: the launch stores its strip's boundary rows into the ring neighbours' halo rows
 // (a separate instantiation so the single-GPU kernel carries none of that epilogue)
-template <int TI, int TJ, int KC, int STAGES, int LV, int OP, bool PEER = false>
-__global__ void __launch_bounds__(TI *TJ * LV)
+template <int TI, int TJ, int KC, int STAGES, int LV, int LP, int OP, bool PEER = false>
+__global__ void __launch_bounds__(TI *TJ * LV, 1)
     mpdata_fused_kernel(const __grid_constant__ CUtensorMap tm_pd,
                         const __grid_constant__ CUtensorMap tm_vn,
                         const __grid_constant__ CUtensorMap tm_wn,
                         const __grid_constant__ CUtensorMap tm_rho, const FusedArgs a) {
-    using C = FusedCfg<TI, TJ, KC, STAGES, LV>;
+    using C = FusedCfg<TI, TJ, KC, STAGES, LV, LP>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * C::kStageBytes);
 
@@ -97,10 +104,11 @@ __global__ void __launch_bounds__(TI *TJ * LV)
     constexpr int sPj = KC + 4, sPi = (TJ + 2) * (KC + 4);
     // vn box [TI+1][3][TJ+1][KC] with origin (i0-1, colour 0, j0-1, k0)
     constexpr int sVc = (TJ + 1) * KC, sVi = 3 * (TJ + 1) * KC;
-    const int oP = (li + 1) * sPi + (lj + 1) * sPj + kl + 2;
-    const int oV = (li + 1) * sVi + (lj + 1) * KC + kl;
-    const int oW = (li * TJ + lj) * (KC + 2) + kl;
-    const int oR = (li * TJ + lj) * KC + kl;
+    const int kq = kl * LP;  // first level of this thread inside the chunk
+    const int oP = (li + 1) * sPi + (lj + 1) * sPj + kq + 2;
+    const int oV = (li + 1) * sVi + (lj + 1) * KC + kq;
+    const int oW = (li * TJ + lj) * (KC + 2) + kq;
+    const int oR = (li * TJ + lj) * KC + kq;
 
     // contiguous unit range of this CTA; unit = tile * chunks + chunk (tile-major)
     const int u_begin = (int)(a.units * blockIdx.x / gridDim.x);
@@ -203,6 +211,78 @@ __global__ void __launch_bounds__(TI *TJ * LV)
         const double *sr = reinterpret_cast<const double *>(smem + stage * C::kStageBytes + C::kRhoOff) + oR;
         const int k0 = chunk * KC;
 
+        if constexpr (LP == 2) {
+            const int k = k0 + kq;  // this thread's level pair (k, k+1)
+            if (vvalid && k < a.K) {
+                const double *P = sp;
+                const double *V = sv;
+                const double2 c = ld2(P);
+                if constexpr (OP == kProbeOp) {  // data-movement probe
+                    const double2 v0 = ld2(V), w01 = ld2(sw), r = ld2(sr);
+                    st2(out + k, make_double2(add(add(c.x, v0.x), add(w01.x, r.x)),
+                                              add(add(c.y, v0.y), add(w01.y, r.y))));
+                    goto next_unit;
+                }
+                const double2 q0 = ld2(P + sPj), q1 = ld2(P + sPi + sPj), q2 = ld2(P + sPi);
+                const double2 q3 = ld2(P - sPj), q4 = ld2(P - sPi - sPj), q5 = ld2(P - sPi);
+                const double2 v0 = ld2(V), v1 = ld2(V + sVc), v2 = ld2(V + 2 * sVc);
+                const double2 v3 = ld2(V - KC), v4 = ld2(V - sVi + sVc - KC), v5 = ld2(V - sVi + 2 * sVc);
+                const double pm = P[-1], pp = P[2];
+                const double2 w01 = ld2(sw);
+                const double w2 = sw[2];
+                const double2 r = ld2(sr);
+                // interfaces k, k+1, k+2 (reference.py:38-60); k+1 is shared by the pair
+                double z0 = fluz_interior(w01.x, pm, c.x);
+                const double z1 = fluz_interior(w01.y, c.x, c.y);
+                double z2 = fluz_interior(w2, c.y, pp);
+                if (chunk == 0 && k == 0) z0 = mul(a.pivbz, z1);
+                const bool pair = k + 1 < a.K;
+                if (chunk == last_chunk && k + 1 == a.K - 1) z2 = mul(a.pivbz, z1);
+                const double z1a = pair ? z1 : mul(a.pivbz, z0);  // k is the top level
+                double acc = 0.0, acd = 0.0;
+                acc = add(mul(sg0, edge_flux<OP>(c.x, q0.x, v0.x)), acc);
+                acd = add(mul(sg0, edge_flux<OP>(c.y, q0.y, v0.y)), acd);
+                acc = add(mul(sg1, edge_flux<OP>(c.x, q1.x, v1.x)), acc);
+                acd = add(mul(sg1, edge_flux<OP>(c.y, q1.y, v1.y)), acd);
+                acc = add(mul(sg2, edge_flux<OP>(c.x, q2.x, v2.x)), acc);
+                acd = add(mul(sg2, edge_flux<OP>(c.y, q2.y, v2.y)), acd);
+                acc = add(mul(sg3, edge_flux<OP>(q3.x, c.x, v3.x)), acc);
+                acd = add(mul(sg3, edge_flux<OP>(q3.y, c.y, v3.y)), acd);
+                acc = add(mul(sg4, edge_flux<OP>(q4.x, c.x, v4.x)), acc);
+                acd = add(mul(sg4, edge_flux<OP>(q4.y, c.y, v4.y)), acd);
+                acc = add(mul(sg5, edge_flux<OP>(q5.x, c.x, v5.x)), acc);
+                acd = add(mul(sg5, edge_flux<OP>(q5.y, c.y, v5.y)), acd);
+                acc = add(acc, sub(z1a, z0));
+                acd = add(acd, sub(z2, z1));
+                double2 val;
+                val.x = sub(c.x, dvd(mul(a.dt, dvd(acc, dual)), r.x));
+                val.y = sub(c.y, dvd(mul(a.dt, dvd(acd, dual)), r.y));
+                double *o = out + k;
+                if (pair) {
+                    st2(o, val);
+                    if (d_row | d_col) {
+                        if (d_row) st2(o + d_row, val);
+                        if (d_col) st2(o + d_col, val);
+                        if (d_row && d_col) st2(o + d_row + d_col, val);
+                    }
+                    if (PEER && peer) {
+                        st2(peer + k, val);
+                        if (d_col) st2(peer + k + d_col, val);
+                    }
+                } else {
+                    o[0] = val.x;
+                    if (d_row | d_col) {
+                        if (d_row) o[d_row] = val.x;
+                        if (d_col) o[d_col] = val.x;
+                        if (d_row && d_col) o[d_row + d_col] = val.x;
+                    }
+                    if (PEER && peer) {
+                        peer[k] = val.x;
+                        if (d_col) peer[k + d_col] = val.x;
+                    }
+                }
+            }
+        } else
 #pragma unroll
         for (int h = 0; h < C::kLevelsPerThread; ++h) {
             const int kk = LV * h;  // level offset of this pass inside the chunk
@@ -258,6 +338,7 @@ __global__ void __launch_bounds__(TI *TJ * LV)
                 }
             }
         }
+    next_unit:
         if (++chunk == a.chunks) {
             chunk = 0;
             if (++tj == a.tiles_j) {
@@ -278,9 +359,9 @@ struct Variant {
     void *peer[2];  // upwind, centred with the fused halo-row stores
 };
 
-template <int TI, int TJ, int KC, int STAGES, int LV = 16>
+template <int TI, int TJ, int KC, int STAGES, int LV = 16, int LP = 1>
 static Variant make_variant() {
-    using C = FusedCfg<TI, TJ, KC, STAGES, LV>;
+    using C = FusedCfg<TI, TJ, KC, STAGES, LV, LP>;
     Variant v;
     v.ti = TI;
     v.tj = TJ;
@@ -288,12 +369,12 @@ static Variant make_variant() {
     v.stages = STAGES;
     v.threads = C::kThreads;
     v.smem = C::kSmemBytes;
-    v.fn[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, TSG_UPWIND>;
-    v.fn[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, TSG_CENTRED>;
-    v.fn[2] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, kProbeOp>;
-    v.fn[3] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, kComputeProbe>;
-    v.peer[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, TSG_UPWIND, true>;
-    v.peer[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, TSG_CENTRED, true>;
+    v.fn[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND>;
+    v.fn[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED>;
+    v.fn[2] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, kProbeOp>;
+    v.fn[3] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, kComputeProbe>;
+    v.peer[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND, true>;
+    v.peer[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED, true>;
     return v;
 }
 
@@ -313,12 +394,17 @@ static Variant *variants(int *count) {
         make_variant<2, 8, 80, 2, 32>(),   // 12: whole 80-level columns, 512 threads
         make_variant<4, 4, 80, 2, 32>(),   // 13: whole 80-level columns, 512 threads
         make_variant<2, 8, 48, 2, 32>(),   // 14: 48-level chunks, 512 threads
+        make_variant<4, 16, 16, 3, 8, 2>(),  // 15 (default): level pairs, 512 threads, 3 x 65.5 KB
+        make_variant<4, 8, 16, 3, 8, 2>(),   // 16: level pairs, 256 threads, 2 CTAs / SM
+        make_variant<2, 16, 16, 2, 8, 2>(),  // 17: level pairs, 256 threads, 2 CTAs / SM
+        make_variant<8, 8, 16, 3, 8, 2>(),   // 18: level pairs, 512 threads, 3 x 63 KB
     };
     *count = (int)(sizeof(v) / sizeof(v[0]));
     return v;
 }
 
-static int g_variant = 1;
+static constexpr int kDefaultVariant = 15;
+static int g_variant = kDefaultVariant;
 
 }  // namespace tsg
 
@@ -328,7 +414,7 @@ extern "C" int tsg_set_fused_variant(int variant) {
     int n = 0;
     variants(&n);
     if (variant < 0 || variant > n) return fail(TSG_EVALUE, "fused variant must be in [0, %d]", n);
-    g_variant = variant == 0 ? 1 : variant;
+    g_variant = variant == 0 ? kDefaultVariant : variant;
     return TSG_OK;
 }
 

@@ -1,7 +1,9 @@
-# A/B timing of fused-kernel builds: bash tools/ab_fused.sh lib1.so lib2.so ... (in-tree build = "cur")
-for i in 1 2 3; do
+# A/B timing of fused-kernel builds: bash tools/ab_fused.sh "variants" lib1.so lib2.so ...
+# (the in-tree build is "cur"; variants are tools/time_fused.py variant ids)
+V=${1:-1}; shift
+for i in 1 2; do
   for l in "$@" cur; do
-    if [ "$l" = cur ]; then python tools/time_fused.py 0 1 | sed "s/^/cur  /"
+    if [ "$l" = cur ]; then python tools/time_fused.py 0 $V | sed "s/^/cur  /"
     else TSG_LIBRARY=$PWD/$l python tools/time_fused.py 0 1 | sed "s|^|$l  |"; fi
   done
 done
