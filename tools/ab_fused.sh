@@ -4,6 +4,6 @@ V=${1:-1}; shift
 for i in 1 2; do
   for l in "$@" cur; do
     if [ "$l" = cur ]; then python tools/time_fused.py 0 $V | sed "s/^/cur  /"
-    else TSG_LIBRARY=$PWD/$l python tools/time_fused.py 0 1 | sed "s|^|$l  |"; fi
+    else TSG_LIBRARY=$PWD/$l python tools/time_fused.py 0 $V | sed "s|^|$l  |"; fi
   done
 done
