@@ -16,7 +16,8 @@
  *        double field[rows + 2][colors][cols + 2][tsg_inner_pitch(inner)]
  *    i.e. (row, colour, column) parallelogram indexing with a one-element periodic
  *    halo ring and the level (or extra) axis innermost and contiguous, padded to an
- *    even count so every element row is 16-byte aligned for TMA / vector access.
+ *    even count so every element row is 16-byte aligned for TMA / vector access (to a
+ *    multiple of 16 for runs of 64 and more: 128-byte aligned, tsg_inner_pitch).
  *    Logical element (i, c, j) sits at storage row i + 1, column j + 1.
  *  - Flat ("indirect") arrays are row-major [n_elements, n_levels] in any numbering,
  *    exactly the reference oracle's convention (reference.py:1-11).
@@ -67,7 +68,8 @@ int tsg_grid_destroy(tsg_grid *g);
  * decomposition): only tsg_fill_hash consults it, so synthetic inputs are identical for
  * every decomposition. */
 int tsg_grid_set_origin(tsg_grid *g, int row0, int global_rows);
-/* Padded innermost extent for `inner` contiguous values per element (1 stays 1). */
+/* Padded innermost extent for `inner` contiguous values per element: 1 stays 1, even
+ * below 64, a multiple of 16 from 64 up (every level run starts on a 128-byte line). */
 int64_t tsg_inner_pitch(int inner);
 /* Number of doubles of a structured field: (rows+2) * colors * (cols+2) * pitch(inner). */
 int64_t tsg_field_elems(const tsg_grid *g, int loc, int inner);

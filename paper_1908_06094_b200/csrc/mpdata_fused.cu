@@ -462,7 +462,8 @@ struct FusedLaunch {
 static int encode_pd(const Variant &v, const tsg_grid *g, const double *pd, CUtensorMap *m) {
     const cuuint64_t pv = (cuuint64_t)pitch_of(g->levels);
     const cuuint64_t W = (cuuint64_t)g->cols + 2, H = (cuuint64_t)g->rows + 2;
-    cuuint64_t dims[3] = {pv, W, H};
+    // extent = the logical levels: the padding past K is zero-filled, never fetched
+    cuuint64_t dims[3] = {(cuuint64_t)g->levels, W, H};
     cuuint64_t str[2] = {pv * 8, W * pv * 8};
     cuuint32_t box[3] = {(cuuint32_t)v.kc + 4, (cuuint32_t)v.tj + 2, (cuuint32_t)v.ti + 2};
     return make_map(m, pd, 3, dims, str, box);
@@ -500,19 +501,19 @@ static int prepare(tsg_grid *g, const double *pd, const double *vn, const double
     const cuuint64_t W = (cuuint64_t)cols + 2, H = (cuuint64_t)rows + 2;
     if (int rc = encode_pd(v, g, pd, &L->m_pd)) return rc;
     {
-        cuuint64_t dims[3] = {pv, W, H};
+        cuuint64_t dims[3] = {(cuuint64_t)K, W, H};
         cuuint64_t str[2] = {pv * 8, W * pv * 8};
         cuuint32_t boxr[3] = {(cuuint32_t)v.kc, (cuuint32_t)v.tj, (cuuint32_t)v.ti};
         if (int rc = make_map(&L->m_rho, rho, 3, dims, str, boxr)) return rc;
     }
     {
-        cuuint64_t dims[4] = {pv, W, 3, H};
+        cuuint64_t dims[4] = {(cuuint64_t)K, W, 3, H};
         cuuint64_t str[3] = {pv * 8, W * pv * 8, 3 * W * pv * 8};
         cuuint32_t box[4] = {(cuuint32_t)v.kc, (cuuint32_t)v.tj + 1, 3, (cuuint32_t)v.ti + 1};
         if (int rc = make_map(&L->m_vn, vn, 4, dims, str, box)) return rc;
     }
     {
-        cuuint64_t dims[3] = {pw, W, H};
+        cuuint64_t dims[3] = {(cuuint64_t)K + 1, W, H};
         cuuint64_t str[2] = {pw * 8, W * pw * 8};
         cuuint32_t box[3] = {(cuuint32_t)v.kc + 2, (cuuint32_t)v.tj, (cuuint32_t)v.ti};
         if (int rc = make_map(&L->m_wn, wn, 3, dims, str, box)) return rc;

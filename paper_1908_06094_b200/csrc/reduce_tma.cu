@@ -168,7 +168,7 @@ static int launch_reduce_tma(const tsg_grid *g, int inner, const double *src, co
     using C = RedCfg<CT>;
     if (int rc = get_encode()) return rc;
     const cuuint64_t p = (cuuint64_t)pitch_of(inner), W = (cuuint64_t)g->cols + 2, H = (cuuint64_t)g->rows + 2;
-    cuuint64_t dims[4] = {p, W, (cuuint64_t)CT, H};
+    cuuint64_t dims[4] = {(cuuint64_t)inner, W, (cuuint64_t)CT, H};
     cuuint64_t str[3] = {p * 8, W * p * 8, CT * W * p * 8};
     cuuint32_t box[4] = {kRedKC, kRedTJ + 2, (cuuint32_t)CT, kRedTI + 2};
     CUtensorMap m;

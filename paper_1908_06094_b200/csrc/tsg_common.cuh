@@ -37,7 +37,13 @@ void clear_error();
     } while (0)
 
 inline int colors_of(int loc) { return loc == TSG_VERTICES ? 1 : (loc == TSG_CELLS ? 2 : 3); }
-__host__ __device__ inline int64_t pitch_of(int inner) { return inner <= 1 ? 1 : ((inner + 1) & ~1); }
+// Innermost (level) pitch: even, so level pairs are 16-byte aligned; from 64 levels up a
+// multiple of 16, so every element's level run starts on a 128-byte line and a 16-level
+// TMA chunk is whole lines (O1280, K = 137: 10.3 vs 10.6 ms per fused step), at <= 19 %
+// padding that the tensor maps never fetch (their level extent is the logical count).
+__host__ __device__ inline int64_t pitch_of(int inner) {
+    return inner <= 1 ? 1 : (inner < 64 ? ((inner + 1) & ~1) : ((inner + 15) & ~15));
+}
 inline bool valid_loc(int loc) { return loc >= 0 && loc <= 2; }
 
 // Index helper for one structured field: [rows+2][colors][cols+2][pitch].

@@ -28,8 +28,10 @@ def require_cuda() -> torch.device:
 
 
 def inner_pitch(inner: int) -> int:
-    """Padded innermost extent (tsg_inner_pitch): even, except 1 stays 1."""
-    return 1 if inner <= 1 else (inner + 1) // 2 * 2
+    """Padded innermost extent (tsg_inner_pitch): 1 stays 1, even below 64, else a multiple of 16."""
+    if inner <= 1:
+        return 1
+    return (inner + 1) // 2 * 2 if inner < 64 else (inner + 15) // 16 * 16
 
 
 class DeviceGrid:

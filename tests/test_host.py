@@ -46,7 +46,10 @@ def test_nm_lists_the_symbols():
 def test_abi_version_and_pitch():
     lib = _lib.lib()
     assert lib.tsg_abi_version() == 1
-    assert [lib.tsg_inner_pitch(n) for n in (1, 2, 3, 6, 80, 81, 137, 138)] == [1, 2, 4, 6, 80, 82, 138, 138]
+    assert [lib.tsg_inner_pitch(n) for n in (1, 2, 3, 6, 63, 64, 80, 81, 137, 138)] == [1, 2, 4, 6, 64, 64, 80, 96, 144, 144]
+    from paper_1908_06094_b200.device import inner_pitch
+
+    assert [inner_pitch(n) for n in (1, 2, 3, 6, 63, 64, 80, 81, 137, 138)] == [1, 2, 4, 6, 64, 64, 80, 96, 144, 144]
 
 
 def test_argument_errors_map_to_reference_exceptions():
