@@ -14,8 +14,11 @@ U[-0.5,0.5) velocities, rho = 1, uniform geometry, dt = 0.1, pivbz = 1).
   preceded (outside the events) by a 256 MiB L2 flush, so no step reads the
   previous step's data from L2.
 * e2e: the same metric through the public flat-array API (StructuredStepper)
-  with pinned host buffers: per step H2D of pd/vn/wn/rho, on-GPU reorder into
-  the structured layout, fused step, reorder back, D2H of pd_out.
+  with pinned host buffers, as the reference's time loop runs it (bench.py:398-403:
+  vn / wn / rho fixed, resident like model weights): per step H2D of the density
+  state pd, on-GPU reorder into the structured layout, fused step, reorder back,
+  D2H of pd_out.  ``e2e_all_inputs`` is the flat oracle call pattern
+  (reference.py:93-116) instead: H2D of pd/vn/wn/rho every step.
 * roofline: algorithmic bytes B_comp per step / average step time, against
   the measured HBM copy bandwidth (MEASURED_PEAKS.json).
 * cpu_baseline / --impl reference: the reference algorithm restated in C
@@ -268,26 +271,35 @@ def run_ours(args):
     # e2e through the public flat API from pinned host buffers (N=1): every step copies its
     # inputs H2D, reorders them into the structured layout, steps, reorders back and copies
     # pd_out D2H; StructuredStepper.run_pipelined overlaps step n+1's H2D with step n's GPU
-    # work and step n-1's D2H (PCIe is full duplex)
-    e2e = None
+    # work and step n-1's D2H (PCIe is full duplex).  Primary: the reference's time loop
+    # (only the density state crosses PCIe, vn / wn / rho stay resident); secondary: the
+    # flat oracle call pattern (every input every step).
+    e2e = e2e_all = None
     if host_fed:
         pinned = [torch.from_numpy(np.ascontiguousarray(inp[n])).pin_memory()
                   for n in ("pd", "vn", "wn", "rho")]
         outs = [torch.empty((V, K), dtype=torch.float64).pin_memory() for _ in range(2)]
-        h2d = sum(t.numel() * 8 for t in pinned)
         d2h = outs[0].numel() * 8
         e2e_steps = max(4, min(args.steps, 40))
-        stepper.run_pipelined([pinned] * 3, outs + outs[:1], DT, PIVBZ)  # warm-up
-        torch.cuda.synchronize()
-        e0, e1 = stepper.run_pipelined([pinned] * e2e_steps, [outs[n % 2] for n in range(e2e_steps)],
-                                       DT, PIVBZ)
-        torch.cuda.synchronize()
-        t_e2e = e0.elapsed_time(e1) / 1e3 / e2e_steps
-        e2e = {"value": V * K / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3,
-               "h2d_gbs": h2d / t_e2e / 1e9,
-               "api": "StructuredStepper.run_pipelined (flat canonical arrays from pinned host "
-                      "memory; H2D, on-GPU reorder, fused step, reorder, D2H every step)"}
+
+        def e2e_run(step_inputs, api):
+            stepper.run_pipelined([pinned] * 3, outs + outs[:1], DT, PIVBZ)  # warm-up (all inputs)
+            torch.cuda.synchronize()
+            e0, e1 = stepper.run_pipelined([step_inputs] * e2e_steps,
+                                           [outs[n % 2] for n in range(e2e_steps)], DT, PIVBZ)
+            torch.cuda.synchronize()
+            t_e2e = e0.elapsed_time(e1) / 1e3 / e2e_steps
+            h2d = sum(t.numel() * 8 for t in step_inputs if t is not None)
+            return {"value": V * K / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3,
+                    "pcie_gbs": (h2d + d2h) / t_e2e / 1e9, "api": api}
+
+        e2e = e2e_run([pinned[0], None, None, None],
+                      "StructuredStepper.run_pipelined, the reference's time loop (bench.py:398-403): "
+                      "per step H2D of the density state pd (flat canonical, pinned), on-GPU reorder, "
+                      "fused step, reorder, D2H of pd_out; vn / wn / rho fixed and resident")
+        e2e_all = e2e_run(pinned, "StructuredStepper.run_pipelined, the flat oracle call pattern "
+                                  "(reference.py:93-116): H2D of pd / vn / wn / rho every step")
 
     if rank != 0:
         if world > 1:
@@ -342,6 +354,7 @@ def run_ours(args):
                      "per": "rank 0's fused launch(es) per step"},
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "e2e_all_inputs": e2e_all,
         "gpu_launches": args.steps * (1 if world == 1 else 3),
         "clocks": clocks.summary(),
         "timed_wall_s": t_wall,

@@ -216,7 +216,9 @@ class StructuredStepper:
         """Many independent host-fed steps with copies overlapped (PCIe is full duplex).
 
         ``inputs[n]`` = (pd, vn, wn, rho) pinned host tensors of step n, ``outputs[n]`` a
-        pinned host tensor receiving that step's pd_out.  Three streams: the H2D copy of
+        pinned host tensor receiving that step's pd_out.  A ``None`` entry keeps that field's
+        resident value (the reference's time loop holds vn / wn / rho fixed, bench.py:398-403:
+        ``(pd, None, None, None)`` moves only the state).  Three streams: the H2D copy of
         step n+1 runs while step n is reordered / advanced on the GPU and step n-1's result
         is copied back; flat staging buffers are double-buffered and guarded by events.
         Returns (start_event, end_event) bracketing all the work.
@@ -243,17 +245,22 @@ class StructuredStepper:
             h2d, comp, d2h = P["h2d"], P["comp"], P["d2h"]
             if packed[b] is not None:
                 h2d.wait_event(packed[b])
+            names = ("pd", "vn", "wn", "rho")
             with torch.cuda.stream(h2d):
-                for k, t in zip(("pd", "vn", "wn", "rho"), src):
-                    P["in"][b][k].copy_(t, non_blocking=True)
+                for k, t in zip(names, src):
+                    if t is not None:
+                        P["in"][b][k].copy_(t, non_blocking=True)
             landed = ev()
             landed.record(h2d)
             comp.wait_event(landed)
             ib = P["in"][b]
-            self._pack(0, K, ib["pd"], self.fwd_v, self.pd, comp)
-            self._pack(2, K, ib["vn"], self.fwd_e, self.vn, comp)
-            self._pack(0, K + 1, ib["wn"], self.fwd_v, self.wn, comp)
-            self._pack(0, K, ib["rho"], self.fwd_v, self.rho, comp)
+            given = dict(zip(names, (t is not None for t in src)))
+            for k, loc, inner, fwd, field in (("pd", 0, K, self.fwd_v, self.pd),
+                                              ("vn", 2, K, self.fwd_e, self.vn),
+                                              ("wn", 0, K + 1, self.fwd_v, self.wn),
+                                              ("rho", 0, K, self.fwd_v, self.rho)):
+                if given[k]:
+                    self._pack(loc, inner, ib[k], fwd, field, comp)
             packed[b] = ev()
             packed[b].record(comp)
             self.step(dt, pivbz, flux_op, stream=comp)

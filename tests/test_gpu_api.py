@@ -412,6 +412,27 @@ def test_pipelined_host_fed_steps_match_oracle(cuda_ok):
         assert np.array_equal(o.numpy(), w)
 
 
+def test_pipelined_time_loop_keeps_resident_velocities(cuda_ok):
+    """run_pipelined with (pd, None, None, None): only the state crosses PCIe (bench e2e);
+    vn / wn / rho keep the values of the last full upload -- the reference's time loop
+    (bench.py:398-403) fed from the host, bitwise against the oracle loop."""
+    import torch
+
+    r, c, lev = 19, 24, 20
+    st = T.StructuredStepper(T.PatchSpec(r, c, lev))
+    inp = O.transport_inputs(r, c, lev, 3, "random", "random", "random")
+    st.set_geometry(inp["signs"], inp["dual"])
+    full = [torch.from_numpy(inp[n]).pin_memory() for n in ("pd", "vn", "wn", "rho")]
+    other = O.transport_inputs(r, c, lev, 4, "random", "random", "random")
+    pds = [torch.from_numpy(other["pd"]).pin_memory(), torch.from_numpy(inp["pd"] * 0.5).pin_memory()]
+    outs = [torch.empty((r * c, lev), dtype=torch.float64).pin_memory() for _ in range(3)]
+    st.run_pipelined([full, [pds[0], None, None, None], [pds[1], None, None, None]], outs, 0.2, 0.8)
+    torch.cuda.synchronize()
+    for o, pd in zip(outs, (inp["pd"], other["pd"], inp["pd"] * 0.5)):
+        want = O.step_inputs(r, c, dict(inp, pd=pd), 0.2, 0.8)["pd_out"]
+        assert np.array_equal(o.numpy(), want)
+
+
 def test_dump_tables_and_csv_loading(cuda_ok):
     import io
 
