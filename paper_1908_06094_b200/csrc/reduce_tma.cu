@@ -4,20 +4,27 @@
 // Same pipeline as the fused MPDATA kernel: a persistent grid walks (TI x TJ tile) x
 // (KC-level chunk) units; one TMA box [TI+2][colours][TJ+2][KC] of the source field (the
 // tile plus its one-ring halo, all target colours) lands in a STAGES-deep shared-memory
-// ring per unit; one thread per (tile position, level) folds every from-colour's
-// neighbours from shared memory in canonical slot order and stores the result (and its
-// periodic halo images) coalesced.  Offsets are compile-time constants of the relation.
+// ring per unit; one thread per (tile position, level pair) folds every from-colour's
+// neighbours from shared memory in canonical slot order (16-byte loads: both levels of the
+// pair at once) and stores the result pair (and its periodic halo images) with one 16-byte
+// store.  Offsets are compile-time constants of the relation.
 #include "tsg_offsets.cuh"
 #include "tsg_tma.cuh"
 
 namespace tsg {
 
-constexpr int kRedTI = 4, kRedTJ = 16, kRedKC = 16, kRedStages = 3;
+constexpr int kRedTJ = 16, kRedKC = 16, kRedStages = 3;
+// tile rows: 8 for cell / edge sources (2-3 colours: 46-69 KB stages, 1024 threads), 4 for
+// vertex sources (a 14 KB stage per 512 threads: several CTAs per SM); measured per relation
+__host__ __device__ constexpr int red_ti(int ct) { return ct == 1 ? 4 : 8; }
+
+constexpr int kRedLanes = kRedKC / 2;  // threads per element: one level pair each
 
 template <int CT>
 struct RedCfg {
-    static constexpr int kThreads = kRedTI * kRedTJ * 16;
-    static constexpr int kBoxBytes = (kRedTI + 2) * CT * (kRedTJ + 2) * kRedKC * 8;
+    static constexpr int TI = red_ti(CT);
+    static constexpr int kThreads = TI * kRedTJ * kRedLanes;
+    static constexpr int kBoxBytes = (TI + 2) * CT * (kRedTJ + 2) * kRedKC * 8;
     static constexpr int kStageBytes = (kBoxBytes + 127) / 128 * 128;
     static constexpr int kSmemBytes = kRedStages * kStageBytes + 128;
 };
@@ -35,15 +42,15 @@ struct RedArgs {
 // sum vn*length / area; MODE 2: weighted cell divergence sum vn*weights[c, n]
 // (mpdata.py:361-376; reference.py:119-134)
 template <int REL, bool SCALE, int MODE = 0>
-__global__ void __launch_bounds__(kRedTI *kRedTJ * 16)
+__global__ void __launch_bounds__(red_ti(loc_colors(REL % 3)) * kRedTJ * kRedLanes)
     reduce_tma_kernel(const __grid_constant__ CUtensorMap tm_src, const RedArgs a) {
     constexpr int CF = loc_colors(REL / 3), CT = loc_colors(REL % 3), W = rel_width(REL);
-    constexpr int TI = kRedTI, TJ = kRedTJ, KC = kRedKC, STAGES = kRedStages;
+    constexpr int TI = red_ti(CT), TJ = kRedTJ, KC = kRedKC, STAGES = kRedStages;
     using C = RedCfg<CT>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * C::kStageBytes);
 
-    const int tid = threadIdx.x, kl = tid & 15, v = tid >> 4;
+    const int tid = threadIdx.x, kl = (tid % kRedLanes) * 2, v = tid / kRedLanes;
     const int li = v / TJ, lj = v % TJ;
     // source box [TI+2][CT][TJ+2][KC], origin (i0-1, colour 0, j0-1, k0)
     constexpr int sJ = KC, sC = (TJ + 2) * KC, sI = CT * (TJ + 2) * KC;
@@ -126,26 +133,42 @@ __global__ void __launch_bounds__(kRedTI *kRedTJ * 16)
             }
         }
         mbar_wait(&bars[stage], (uint32_t)((n / STAGES) & 1));
-        const int k = chunk * KC + kl;
+        const int k = chunk * KC + kl;  // this thread's level pair (k, k+1)
         if (valid && k < a.nk) {
             const double *S = reinterpret_cast<const double *>(smem + stage * C::kStageBytes) + oS;
+            const bool pair = k + 1 < a.nk;
 #pragma unroll
             for (int c = 0; c < CF; ++c) {
-                double acc = 0.0;
+                double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
                 for (int s = 0; s < W; ++s) {
-                    const double x = S[rel_off(REL, c, s, 0) * sI + rel_off(REL, c, s, 1) * sC +
-                                       rel_off(REL, c, s, 2) * sJ];
-                    acc = MODE ? add(mul(x, w[c][s]), acc) : add(x, acc);
+                    const double2 x = ld2(S + rel_off(REL, c, s, 0) * sI + rel_off(REL, c, s, 1) * sC +
+                                          rel_off(REL, c, s, 2) * sJ);
+                    if (MODE) {
+                        acc.x = add(mul(x.x, w[c][s]), acc.x);
+                        acc.y = add(mul(x.y, w[c][s]), acc.y);
+                    } else {
+                        acc.x = add(x.x, acc.x);
+                        acc.y = add(x.y, acc.y);
+                    }
                 }
-                if (SCALE) acc = mul(acc, sc[c]);
-                if (MODE == 1) acc = dvd(acc, sc[c]);
+                if (SCALE) acc = make_double2(mul(acc.x, sc[c]), mul(acc.y, sc[c]));
+                if (MODE == 1) acc = make_double2(dvd(acc.x, sc[c]), dvd(acc.y, sc[c]));
                 double *o = out[c] + k;
-                o[0] = acc;
-                if (dr | dc) {
-                    if (dr) o[dr] = acc;
-                    if (dc) o[dc] = acc;
-                    if (dr && dc) o[dr + dc] = acc;
+                if (pair) {
+                    st2(o, acc);
+                    if (dr | dc) {
+                        if (dr) st2(o + dr, acc);
+                        if (dc) st2(o + dc, acc);
+                        if (dr && dc) st2(o + dr + dc, acc);
+                    }
+                } else {  // odd level count: the last level alone
+                    o[0] = acc.x;
+                    if (dr | dc) {
+                        if (dr) o[dr] = acc.x;
+                        if (dc) o[dc] = acc.x;
+                        if (dr && dc) o[dr + dc] = acc.x;
+                    }
                 }
             }
         }
@@ -170,7 +193,7 @@ static int launch_reduce_tma(const tsg_grid *g, int inner, const double *src, co
     const cuuint64_t p = (cuuint64_t)pitch_of(inner), W = (cuuint64_t)g->cols + 2, H = (cuuint64_t)g->rows + 2;
     cuuint64_t dims[4] = {(cuuint64_t)inner, W, (cuuint64_t)CT, H};
     cuuint64_t str[3] = {p * 8, W * p * 8, CT * W * p * 8};
-    cuuint32_t box[4] = {kRedKC, kRedTJ + 2, (cuuint32_t)CT, kRedTI + 2};
+    cuuint32_t box[4] = {kRedKC, kRedTJ + 2, (cuuint32_t)CT, (cuuint32_t)C::TI + 2};
     CUtensorMap m;
     if (int rc = make_map(&m, src, 4, dims, str, box)) return rc;
     RedArgs a;
@@ -185,7 +208,7 @@ static int launch_reduce_tma(const tsg_grid *g, int inner, const double *src, co
     a.flags = g->flags;
     a.tiles_j = (g->cols + kRedTJ - 1) / kRedTJ;
     a.chunks = (inner + kRedKC - 1) / kRedKC;
-    a.units = (int64_t)((g->rows + kRedTI - 1) / kRedTI) * a.tiles_j * a.chunks;
+    a.units = (int64_t)((g->rows + C::TI - 1) / C::TI) * a.tiles_j * a.chunks;
     if (a.units >= (1LL << 31)) return fail(TSG_EVALUE, "field too large for one reduce launch");
     void *fn = (void *)reduce_tma_kernel<REL, SCALE, MODE>;
     TSG_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));

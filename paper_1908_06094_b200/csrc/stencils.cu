@@ -102,6 +102,51 @@ __global__ void __launch_bounds__(256) reduce_indirect_kernel(const int64_t *__r
     }
 }
 
+// Table-driven reduce for an even level count: one thread per (row, level pair) item,
+// items flattened over the whole table so every lane is busy whatever the level count, and
+// kUnroll items per thread per pass with all their gathers issued before any sum -- the
+// gather is latency-bound otherwise (measured: 3.1 TB/s, 29 % issue, 50 % occupancy with
+// one warp per row).  Lanes of one row share its table entries (broadcast loads) and read
+// consecutive 16-byte pairs of each neighbour row (coalesced).
+constexpr int kUnroll = 4;
+
+template <int W>
+__global__ void __launch_bounds__(256) reduce_indirect_pairs_kernel(
+    const int64_t *__restrict__ table, uint32_t nitems, FastDiv npairs, int nlev,
+    const double *__restrict__ src, const double *__restrict__ scale, double *__restrict__ dst) {
+    const uint32_t T = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < nitems; base += kUnroll * T) {
+        double2 v[kUnroll][W];
+        double sc[kUnroll];
+        uint32_t row[kUnroll], kp[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint32_t it = base + u * T;
+            row[u] = npairs.div(it < nitems ? it : 0);
+            kp[u] = 2 * (it - row[u] * npairs.d);
+            if (it < nitems) {
+                sc[u] = scale ? __ldg(scale + row[u]) : 1.0;
+#pragma unroll
+                for (int s = 0; s < W; ++s)
+                    v[u][s] = __ldg(reinterpret_cast<const double2 *>(
+                        src + __ldg(table + (int64_t)row[u] * W + s) * nlev + kp[u]));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (base + u * T >= nitems) break;
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int s = 0; s < W; ++s) {
+                acc.x = add(v[u][s].x, acc.x);
+                acc.y = add(v[u][s].y, acc.y);
+            }
+            if (scale) acc = make_double2(mul(acc.x, sc[u]), mul(acc.y, sc[u]));
+            st2(dst + (int64_t)row[u] * nlev + kp[u], acc);
+        }
+    }
+}
+
 // -- cell divergence (mpdata.py:361-416, reference.py:119-134) --------------------------
 
 template <bool WEIGHTED>
@@ -310,7 +355,8 @@ extern "C" int tsg_neighbor_reduce(const tsg_grid *g, int from_loc, int to_loc, 
     cudaStream_t st = (cudaStream_t)s;
     const int rel = from_loc * 3 + to_loc;
     // long level runs: the TMA-staged tile kernel (reduce_tma.cu); short ones: element lines
-    if (inner >= 16 && (reinterpret_cast<uintptr_t>(src) % 16) == 0)
+    if (inner >= 16 && (reinterpret_cast<uintptr_t>(src) % 16) == 0 &&
+        (reinterpret_cast<uintptr_t>(dst) % 16) == 0)
         return reduce_tma(g, rel, inner, src, scale, dst, st);
     const int64_t lines = (int64_t)g->rows * Fd.colors;
 #define TSG_REDUCE_CASE(R)                                                                        \
@@ -341,6 +387,28 @@ extern "C" int tsg_neighbor_reduce_indirect(const int64_t *table, int64_t nrows,
     if (nrows == 0) return TSG_OK;
     const int sms = sm_count();
     cudaStream_t st = (cudaStream_t)s;
+    const int64_t nitems = nrows * (int64_t)(nlev / 2);
+    const bool aligned = (reinterpret_cast<uintptr_t>(src) % 16) == 0 &&
+                         (reinterpret_cast<uintptr_t>(dst) % 16) == 0;
+    if ((nlev & 1) == 0 && aligned && nitems < (1LL << 31) && (width == 2 || width == 3 || width == 4 || width == 6)) {
+        const FastDiv np((uint32_t)(nlev / 2));
+        auto go = [&](auto kernel) {
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
+            int64_t blocks = (int64_t)sms * (per_sm < 1 ? 1 : per_sm);
+            const int64_t need = (nitems + 256 * kUnroll - 1) / (256 * kUnroll);
+            if (blocks > need) blocks = need;
+            kernel<<<(unsigned)blocks, 256, 0, st>>>(table, (uint32_t)nitems, np, nlev, src, scale, dst);
+        };
+        switch (width) {
+            case 2: go(reduce_indirect_pairs_kernel<2>); break;
+            case 3: go(reduce_indirect_pairs_kernel<3>); break;
+            case 4: go(reduce_indirect_pairs_kernel<4>); break;
+            default: go(reduce_indirect_pairs_kernel<6>); break;
+        }
+        TSG_CHECK_LAUNCH();
+        return TSG_OK;
+    }
     switch (width) {
         case 2: launch_rows(reduce_indirect_kernel<2>, nrows, sms, st, table, nrows, width, nlev, src, scale, dst); break;
         case 3: launch_rows(reduce_indirect_kernel<3>, nrows, sms, st, table, nrows, width, nlev, src, scale, dst); break;
@@ -361,7 +429,8 @@ extern "C" int tsg_cell_divergence(const tsg_grid *g, int weighted, const double
     int K = g->levels;
     FieldIx Fvn(g->rows, g->cols, 3, K), Fl(g->rows, g->cols, 3, 1), Fa(g->rows, g->cols, 2, 1),
         Fw(g->rows, g->cols, 2, 3), Fo(g->rows, g->cols, 2, K);
-    if (K >= 16 && (reinterpret_cast<uintptr_t>(vn) % 16) == 0)
+    if (K >= 16 && (reinterpret_cast<uintptr_t>(vn) % 16) == 0 &&
+        (reinterpret_cast<uintptr_t>(out) % 16) == 0)
         return cell_divergence_tma(g, weighted, vn, length, area, weights, out, (cudaStream_t)s);
     if (weighted)
         launch_lines(cell_div_kernel<true>, g->cols, 2LL * g->rows, g->num_sms, (cudaStream_t)s, Fvn,

@@ -482,6 +482,27 @@ def test_device_resident_results_follow_the_staleness_contract(cuda_ok):
     assert np.array_equal(T.field_to_flat(state.pd_out), want["pd_out"])
 
 
+@pytest.mark.parametrize("shape", [(13, 21, 20), (6, 37, 33), (9, 10, 2)])
+def test_indirect_reduce_every_width(cuda_ok, shape):
+    """The table-driven gather (flattened level-pair items for even level counts, one warp
+    per row otherwise) for the nine relations' widths 2 / 3 / 4 / 6, plain and scaled, in a
+    Hilbert / colour-interleaved numbering, against the oracle bitwise."""
+    r, c, lev = shape
+    spec = T.PatchSpec(r, c, lev)
+    rng = np.random.default_rng(lev + 1)
+    for (f, t) in T.OFFSET_TABLES:
+        pf = T.make_permutation(T.Numbering.UN, spec, f)
+        pt = T.make_permutation(T.Numbering.UN, spec, t)
+        table = T.build_neighbor_table(spec, f, t, pf, pt)
+        a = rng.random((T.element_count(spec, t), lev))
+        fac = 0.5 + rng.random((T.element_count(spec, f), 1))
+        a_perm = a[pt.inverse]
+        want = O.neighbor_sum(table.ids, a_perm)
+        assert np.array_equal(T.run_neighbor_sum(table, a_perm), want), (f, t)
+        want_s = O.neighbor_sum_scaled(table.ids, a_perm, fac)
+        assert np.array_equal(T.run_neighbor_sum_scaled(table, a_perm, fac), want_s), (f, t)
+
+
 @pytest.mark.parametrize("shape", [(13, 21, 20), (6, 37, 33)])
 def test_tma_reduce_and_cell_divergence_paths(cuda_ok, shape):
     """Long level runs take the TMA-staged kernels (reduce_tma.cu): all nine relations,
