@@ -75,6 +75,66 @@ __global__ void __launch_bounds__(256) unpack_lines_kernel(FieldIx F, int inner,
     }
 }
 
+// level-pair item variants for even level counts: one thread per (element, level pair),
+// items flattened over the field so every lane is busy whatever the level count, with
+// kItemUnroll items per thread in flight (the element-line kernels leave 24 of 32 lanes
+// idle in the second pass of an 80-level run and are latency-bound).
+constexpr int kItemUnroll = 4;
+
+__global__ void __launch_bounds__(256) pack_pairs_kernel(FieldIx F, int inner, PointDec D,
+                                                         const double *__restrict__ flat,
+                                                         const int64_t *__restrict__ forward,
+                                                         double *__restrict__ f, int flags) {
+    const uint32_t T = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < D.n; base += kItemUnroll * T) {
+        double2 v[kItemUnroll];
+        Pt p[kItemUnroll];
+#pragma unroll
+        for (int u = 0; u < kItemUnroll; ++u) {
+            const uint32_t t = base + u * T;
+            if (t < D.n) {
+                p[u] = decompose(t, D);
+                const int64_t rank = forward ? __ldg(forward + p[u].e) : p[u].e;
+                v[u] = __ldg(reinterpret_cast<const double2 *>(flat + rank * inner + 2 * p[u].k));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kItemUnroll; ++u) {
+            if (base + u * T >= D.n) break;
+            put2(f + F.at(p[u].i, p[u].c, p[u].j), images(F, p[u].i, p[u].j, flags), 2 * p[u].k, v[u]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) unpack_pairs_kernel(FieldIx F, int inner, PointDec D,
+                                                           const double *__restrict__ f,
+                                                           const int64_t *__restrict__ forward,
+                                                           double *__restrict__ flat) {
+    const uint32_t T = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < D.n; base += kItemUnroll * T) {
+        double2 v[kItemUnroll];
+        Pt p[kItemUnroll];
+#pragma unroll
+        for (int u = 0; u < kItemUnroll; ++u) {
+            const uint32_t t = base + u * T;
+            if (t < D.n) {
+                p[u] = decompose(t, D);
+                v[u] = __ldg(reinterpret_cast<const double2 *>(f + F.at(p[u].i, p[u].c, p[u].j) + 2 * p[u].k));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kItemUnroll; ++u) {
+            if (base + u * T >= D.n) break;
+            const int64_t rank = forward ? __ldg(forward + p[u].e) : p[u].e;
+            st2(flat + rank * inner + 2 * p[u].k, v[u]);
+        }
+    }
+}
+
+static bool pairs_ok(int inner, const void *flat) {
+    return inner >= 16 && (inner & 1) == 0 && (reinterpret_cast<uintptr_t>(flat) % 16) == 0;
+}
+
 // -- periodic halo (executors.py:74-86): rows then columns, corners wrap both ways ----
 
 __global__ void halo_kernel(FieldIx F, int inner, double *__restrict__ f, int flags) {
@@ -406,7 +466,11 @@ extern "C" int tsg_pack(const tsg_grid *g, int loc, int inner, const double *fla
     FieldIx F(g->rows, g->cols, colors_of(loc), inner);
     if (!PointDec::fits(g->rows, g->cols, F.colors, inner)) return fail(TSG_EVALUE, "field too large");
     PointDec D(g->rows, g->cols, F.colors, inner);
-    if (inner >= 16)
+    if (pairs_ok(inner, flat)) {
+        PointDec Dp(g->rows, g->cols, F.colors, inner / 2);
+        pack_pairs_kernel<<<grid_for((Dp.n + kItemUnroll - 1) / kItemUnroll, 256, g->num_sms), 256, 0,
+                            (cudaStream_t)s>>>(F, inner, Dp, flat, forward, field, g->flags);
+    } else if (inner >= 16)
         launch_lines(pack_lines_kernel, g->cols, (int64_t)g->rows * F.colors, g->num_sms,
                      (cudaStream_t)s, F, inner, flat, forward, field, g->flags);
     else
@@ -424,7 +488,11 @@ extern "C" int tsg_unpack(const tsg_grid *g, int loc, int inner, const double *f
     FieldIx F(g->rows, g->cols, colors_of(loc), inner);
     if (!PointDec::fits(g->rows, g->cols, F.colors, inner)) return fail(TSG_EVALUE, "field too large");
     PointDec D(g->rows, g->cols, F.colors, inner);
-    if (inner >= 16)
+    if (pairs_ok(inner, flat)) {
+        PointDec Dp(g->rows, g->cols, F.colors, inner / 2);
+        unpack_pairs_kernel<<<grid_for((Dp.n + kItemUnroll - 1) / kItemUnroll, 256, g->num_sms), 256, 0,
+                              (cudaStream_t)s>>>(F, inner, Dp, field, forward, flat);
+    } else if (inner >= 16)
         launch_lines(unpack_lines_kernel, g->cols, (int64_t)g->rows * F.colors, g->num_sms,
                      (cudaStream_t)s, F, inner, field, forward, flat);
     else

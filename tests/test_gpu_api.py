@@ -222,14 +222,15 @@ def test_cell_divergence_and_weights(cuda_ok, golden):
         assert np.array_equal(T.field_to_flat(out), golden[f"cdiv_{int(weighted)}"])
 
 
-def test_pack_unpack_roundtrip_every_numbering(cuda_ok):
+@pytest.mark.parametrize("levels", [5, 20])  # element lines / flattened level-pair items
+def test_pack_unpack_roundtrip_every_numbering(cuda_ok, levels):
     import torch
 
-    spec = T.PatchSpec(9, 7, 5)
+    spec = T.PatchSpec(9, 7, levels)
     for loc in L:
         f = T.make_storage(spec, loc, "x")
         n = T.element_count(spec, loc)
-        vals = torch.rand((n, 5), dtype=torch.float64, device="cuda")
+        vals = torch.rand((n, levels), dtype=torch.float64, device="cuda")
         for num in T.Numbering:
             if num is T.Numbering.HN and loc is L.EDGES:
                 continue
