@@ -4,6 +4,8 @@
 // level axis fastest, so every neighbour read is a contiguous run of a neighbouring
 // element's level column (coalesced; neighbour reuse is served by L1/L2).  Grids are a
 // multiple of the SM count with grid-stride loops.
+#include <algorithm>
+
 #include "tsg_common.cuh"
 #include "tsg_offsets.cuh"
 
@@ -264,6 +266,101 @@ __global__ void __launch_bounds__(256) advance_kernel(FieldIx Fv, int K, double 
     }
 }
 
+// Level-pair item forms of the four unfused stages: one thread per
+// (element, level pair) over the whole field, kUnroll items per thread per pass, 16-byte
+// loads and stores -- the element-line forms above are latency-bound with a quarter of
+// their lanes idle in the last pass of an 80-level run.
+#define TSG_ITEMS(base, u, D)                                                                  \
+    for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x, T_ = gridDim.x * blockDim.x;   \
+         base < (D).n; base += kUnroll * T_)                                                     \
+        _Pragma("unroll") for (int u = 0; u < kUnroll; ++u)                                     \
+            if (base + u * T_ < (D).n)
+
+template <int OP>
+__global__ void __launch_bounds__(256) flux_pairs_kernel(FieldIx Fp, FieldIx Fe, PointDec D,
+                                                         const double *__restrict__ pd,
+                                                         const double *__restrict__ vn,
+                                                         double *__restrict__ flux, int flags) {
+    TSG_ITEMS(base, u, D) {
+        const Pt e = decompose(base + u * T_, D);
+        const int k = 2 * e.k;
+        // E->V slot 1 (connectivity.py:38-42): c0 (0,+1), c1 (+1,+1), c2 (+1,0)
+        const double2 po = ld2(pd + Fp.at(e.i, 0, e.j) + k);
+        const double2 pp = ld2(pd + Fp.at(e.i + (e.c == 0 ? 0 : 1), 0, e.j + (e.c == 2 ? 0 : 1)) + k);
+        const double2 v = ld2(vn + Fe.at(e.i, e.c, e.j) + k);
+        put2(flux + Fe.at(e.i, e.c, e.j), images(Fe, e.i, e.j, flags), k,
+             make_double2(edge_flux<OP>(po.x, pp.x, v.x), edge_flux<OP>(po.y, pp.y, v.y)));
+    }
+}
+
+// interface pairs (2p, 2p+1) over 0..K; the partner of the last interface is padding (0)
+__global__ void __launch_bounds__(256) fluz_pairs_kernel(FieldIx Fp, FieldIx Fw, PointDec D, int K,
+                                                         double pivbz, const double *__restrict__ pd,
+                                                         const double *__restrict__ wn,
+                                                         double *__restrict__ fluz, int flags) {
+    TSG_ITEMS(base, u, D) {
+        const Pt e = decompose(base + u * T_, D);
+        const double *P = pd + Fp.at(e.i, 0, e.j), *W = wn + Fw.at(e.i, 0, e.j);
+        double f[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int k = 2 * e.k + h;
+            if (k == 0) f[h] = mul(pivbz, fluz_interior(W[1], P[0], P[1]));
+            else if (k == K) f[h] = mul(pivbz, fluz_interior(W[K - 1], P[K - 2], P[K - 1]));
+            else if (k > K) f[h] = 0.0;
+            else f[h] = fluz_interior(W[k], P[k - 1], P[k]);
+        }
+        put2(fluz + Fw.at(e.i, 0, e.j), images(Fw, e.i, e.j, flags), 2 * e.k, make_double2(f[0], f[1]));
+    }
+}
+
+__global__ void __launch_bounds__(256) div_pairs_kernel(FieldIx Fe, FieldIx Fw, FieldIx Fs, FieldIx Fd,
+                                                        FieldIx Fv, PointDec D,
+                                                        const double *__restrict__ flux,
+                                                        const double *__restrict__ fluz,
+                                                        const double *__restrict__ signs,
+                                                        const double *__restrict__ dual,
+                                                        double *__restrict__ divvd, int flags) {
+    constexpr int REL = TSG_VERTICES * 3 + TSG_EDGES;
+    TSG_ITEMS(base, u, D) {
+        const Pt e = decompose(base + u * T_, D);
+        const int k = 2 * e.k;
+        const double *S = signs + Fs.at(e.i, 0, e.j);
+        const double *Z = fluz + Fw.at(e.i, 0, e.j);
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int s = 0; s < 6; ++s) {
+            const int8_t *o = c_offsets[REL][0][s];
+            const double2 f = ld2(flux + Fe.at(e.i + o[0], o[1], e.j + o[2]) + k);
+            const double sg = __ldg(S + s);
+            acc.x = add(mul(sg, f.x), acc.x);
+            acc.y = add(mul(sg, f.y), acc.y);
+        }
+        const double2 z01 = ld2(Z + k);
+        const double z2 = Z[k + 2];
+        acc.x = add(acc.x, sub(z01.y, z01.x));
+        acc.y = add(acc.y, sub(z2, z01.y));
+        const double du = __ldg(dual + Fd.at(e.i, 0, e.j));
+        put2(divvd + Fv.at(e.i, 0, e.j), images(Fv, e.i, e.j, flags), k,
+             make_double2(dvd(acc.x, du), dvd(acc.y, du)));
+    }
+}
+
+__global__ void __launch_bounds__(256) advance_pairs_kernel(FieldIx Fv, PointDec D, double dt,
+                                                            const double *__restrict__ pd,
+                                                            const double *__restrict__ divvd,
+                                                            const double *__restrict__ rho,
+                                                            double *__restrict__ pd_out, int flags) {
+    TSG_ITEMS(base, u, D) {
+        const Pt e = decompose(base + u * T_, D);
+        const int64_t q = Fv.at(e.i, 0, e.j) + 2 * e.k;
+        const double2 d = ld2(divvd + q), r = ld2(rho + q), p = ld2(pd + q);
+        put2(pd_out + Fv.at(e.i, 0, e.j), images(Fv, e.i, e.j, flags), 2 * e.k,
+             make_double2(sub(p.x, dvd(mul(dt, d.x), r.x)), sub(p.y, dvd(mul(dt, d.y), r.y))));
+    }
+}
+#undef TSG_ITEMS
+
 // -- indirect (table-driven) MPDATA over flat arrays (reference.py:93-116) -------------
 
 #define TSG_FLAT_ROWS(r, n)                                                          \
@@ -464,6 +561,23 @@ extern "C" int tsg_mpdata_step_unfused(const tsg_grid *g, const double *pd, cons
         Fs(g->rows, g->cols, 1, 6), Fd(g->rows, g->cols, 1, 1);
     const int C = g->cols, sms = g->num_sms;
     const int64_t lE = 3LL * g->rows, lV = g->rows;
+    if (PointDec::fits(g->rows, C, 3, K + 1)) {  // level-pair items
+        // an odd level count's last pair ends in the padding of every field (even pitch)
+        const int np = (K + 1) / 2;
+        const PointDec DE(g->rows, C, 3, np), DV(g->rows, C, 1, np), DZ(g->rows, C, 1, K / 2 + 1);
+        auto blocks = [&](const PointDec &D) { return (unsigned)std::min<int64_t>(
+            (D.n + 256 * kUnroll - 1) / (256 * kUnroll), (int64_t)sms * 8); };
+        if (flux_op == TSG_UPWIND)
+            flux_pairs_kernel<TSG_UPWIND><<<blocks(DE), 256, 0, st>>>(Fv, Fe, DE, pd, vn, flux, g->flags);
+        else
+            flux_pairs_kernel<TSG_CENTRED><<<blocks(DE), 256, 0, st>>>(Fv, Fe, DE, pd, vn, flux, g->flags);
+        fluz_pairs_kernel<<<blocks(DZ), 256, 0, st>>>(Fv, Fw, DZ, K, pivbz, pd, wn, fluz, g->flags);
+        div_pairs_kernel<<<blocks(DV), 256, 0, st>>>(Fe, Fw, Fs, Fd, Fv, DV, flux, fluz, signs, dual, divvd,
+                                                     g->flags);
+        advance_pairs_kernel<<<blocks(DV), 256, 0, st>>>(Fv, DV, dt, pd, divvd, rho, pd_out, g->flags);
+        TSG_CHECK_LAUNCH();
+        return TSG_OK;
+    }
     if (flux_op == TSG_UPWIND)
         launch_lines(flux_kernel<TSG_UPWIND>, C, lE, sms, st, Fv, Fe, K, pd, vn, flux, g->flags);
     else

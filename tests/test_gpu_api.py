@@ -363,7 +363,7 @@ def test_o1280_class_properties(cuda_ok):
     flux, fluz, div = g.empty(2, K), g.empty(0, K + 1), g.empty(0, K)
     _lib.call("tsg_mpdata_step_unfused", g.handle, *ins, _lib.ptr(flux), _lib.ptr(fluz), _lib.ptr(div),
               _lib.ptr(b), 0.05, 0.0, 0, s)
-    assert torch.equal(a, b)
+    assert torch.equal(a[..., :K], b[..., :K])  # the level padding is not field content
     work = torch.empty(1026, dtype=torch.float64, device="cuda")
     _lib.call("tsg_total_mass", g.handle, _lib.ptr(fields["pd"]), _lib.ptr(dual), _lib.ptr(work[:1024]),
               _lib.ptr(work[1024:1025]), s)
