@@ -427,6 +427,83 @@ __global__ void __launch_bounds__(256) idiv_advance_kernel(
     }
 }
 
+// Level-pair item forms of the table-driven step (even level counts: 16-byte aligned flat
+// rows): one thread per (row, level pair), kUnroll items in flight per thread.
+#define TSG_FLAT_ITEMS(it, u, n)                                                              \
+    for (uint32_t base_ = blockIdx.x * blockDim.x + threadIdx.x, T_ = gridDim.x * blockDim.x;  \
+         base_ < (n); base_ += kUnroll * T_)                                                    \
+        _Pragma("unroll") for (int u = 0; u < kUnroll; ++u)                                    \
+            for (uint32_t it = base_ + u * T_; it < (n); it = (n))
+
+template <int OP>
+__global__ void __launch_bounds__(256) iflux_pairs_kernel(const int64_t *__restrict__ e2v, uint32_t n,
+                                                          FastDiv np, int K, const double *__restrict__ pd,
+                                                          const double *__restrict__ vn,
+                                                          double *__restrict__ flux) {
+    TSG_FLAT_ITEMS(it, u, n) {
+        const uint32_t e = np.div(it);
+        const int k = 2 * (it - e * np.d);
+        const double2 po = ld2(pd + __ldg(e2v + 2 * (int64_t)e) * K + k);
+        const double2 pp = ld2(pd + __ldg(e2v + 2 * (int64_t)e + 1) * K + k);
+        const double2 v = ld2(vn + (int64_t)e * K + k);
+        st2(flux + (int64_t)e * K + k,
+            make_double2(edge_flux<OP>(po.x, pp.x, v.x), edge_flux<OP>(po.y, pp.y, v.y)));
+    }
+}
+
+// interfaces in pairs over 0..K of a K+1-wide row (odd width: the last item is a single)
+__global__ void __launch_bounds__(256) ifluz_pairs_kernel(uint32_t n, FastDiv np, int K, double pivbz,
+                                                          const double *__restrict__ pd,
+                                                          const double *__restrict__ wn,
+                                                          double *__restrict__ fluz) {
+    TSG_FLAT_ITEMS(it, u, n) {
+        const uint32_t v = np.div(it);
+        const int k0 = 2 * (it - v * np.d);
+        const double *P = pd + (int64_t)v * K, *W = wn + (int64_t)v * (K + 1);
+        double *o = fluz + (int64_t)v * (K + 1);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int k = k0 + h;
+            if (k > K) break;
+            double f;
+            if (k == 0) f = mul(pivbz, fluz_interior(W[1], P[0], P[1]));
+            else if (k == K) f = mul(pivbz, fluz_interior(W[K - 1], P[K - 2], P[K - 1]));
+            else f = fluz_interior(W[k], P[k - 1], P[k]);
+            o[k] = f;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) idiv_advance_pairs_kernel(
+    const int64_t *__restrict__ v2e, uint32_t n, FastDiv np, int K, double dt,
+    const double *__restrict__ signs, const double *__restrict__ dual, const double *__restrict__ flux,
+    const double *__restrict__ fluz, const double *__restrict__ pd, const double *__restrict__ rho,
+    double *__restrict__ div, double *__restrict__ pd_out) {
+    TSG_FLAT_ITEMS(it, u, n) {
+        const uint32_t v = np.div(it);
+        const int k = 2 * (it - v * np.d);
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int s = 0; s < 6; ++s) {
+            const double2 f = ld2(flux + __ldg(v2e + (int64_t)v * 6 + s) * K + k);
+            const double sg = __ldg(signs + (int64_t)v * 6 + s);
+            acc.x = add(mul(sg, f.x), acc.x);
+            acc.y = add(mul(sg, f.y), acc.y);
+        }
+        const double *Z = fluz + (int64_t)v * (K + 1) + k;  // odd row width: scalar loads
+        const double z0 = Z[0], z1 = Z[1], z2 = Z[2];
+        acc.x = add(acc.x, sub(z1, z0));
+        acc.y = add(acc.y, sub(z2, z1));
+        const double du = __ldg(dual + v);
+        const double2 d = make_double2(dvd(acc.x, du), dvd(acc.y, du));
+        const int64_t q = (int64_t)v * K + k;
+        st2(div + q, d);
+        const double2 r = ld2(rho + q), p = ld2(pd + q);
+        st2(pd_out + q, make_double2(sub(p.x, dvd(mul(dt, d.x), r.x)), sub(p.y, dvd(mul(dt, d.y), r.y))));
+    }
+}
+#undef TSG_FLAT_ITEMS
+
 }  // namespace tsg
 
 using namespace tsg;
@@ -602,6 +679,23 @@ extern "C" int tsg_transport_indirect(const int64_t *e2v, const int64_t *v2e, co
     if (nv < 1 || ne < 1) return fail(TSG_EVALUE, "empty mesh (nv=%lld, ne=%lld)", (long long)nv, (long long)ne);
     cudaStream_t st = (cudaStream_t)s;
     const int sms = sm_count();
+    auto a16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) % 16) == 0; };
+    if ((nlev & 1) == 0 && ne * (nlev / 2) < (1LL << 31) && nv * (nlev / 2 + 1) < (1LL << 31) &&
+        a16(pd) && a16(vn) && a16(rho) && a16(flux) && a16(div) && a16(pd_out)) {
+        const int np = nlev / 2;
+        const uint32_t nE = (uint32_t)(ne * np), nV = (uint32_t)(nv * np), nZ = (uint32_t)(nv * (np + 1));
+        auto blocks = [&](uint32_t n) { return (unsigned)std::min<int64_t>(
+            ((int64_t)n + 256 * kUnroll - 1) / (256 * kUnroll), (int64_t)sms * 8); };
+        if (flux_op == TSG_UPWIND)
+            iflux_pairs_kernel<TSG_UPWIND><<<blocks(nE), 256, 0, st>>>(e2v, nE, FastDiv(np), nlev, pd, vn, flux);
+        else
+            iflux_pairs_kernel<TSG_CENTRED><<<blocks(nE), 256, 0, st>>>(e2v, nE, FastDiv(np), nlev, pd, vn, flux);
+        ifluz_pairs_kernel<<<blocks(nZ), 256, 0, st>>>(nZ, FastDiv(np + 1), nlev, pivbz, pd, wn, fluz);
+        idiv_advance_pairs_kernel<<<blocks(nV), 256, 0, st>>>(v2e, nV, FastDiv(np), nlev, dt, signs, dual,
+                                                              flux, fluz, pd, rho, div, pd_out);
+        TSG_CHECK_LAUNCH();
+        return TSG_OK;
+    }
     if (flux_op == TSG_UPWIND)
         launch_rows(iflux_kernel<TSG_UPWIND>, ne, sms, st, e2v, ne, nlev, pd, vn, flux);
     else

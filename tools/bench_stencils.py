@@ -143,6 +143,21 @@ def fusion(rows, cols, K):
                                  _lib.ptr(div), _lib.ptr(out), 0.1, 1.0, 0, s()))
     record("mpdata_unfused", t2, unfused_bytes, patch=[rows, cols, K], updates_per_s=v * K / t2,
            fused_speedup=t2 / t, bytes_ratio=unfused_bytes / fused_bytes)
+    if K % 2 or rows * cols > 1 << 20:
+        return
+    # the flat oracle API (reference.py:93-116) through the table-driven kernels, SN order
+    e2v = build_neighbor_table(PatchSpec(rows, cols, K), L.EDGES, L.VERTICES, as_tensor=True).ids
+    v2e = build_neighbor_table(PatchSpec(rows, cols, K), L.VERTICES, L.EDGES, as_tensor=True).ids
+    fl = {n: torch.rand((cnt, w), dtype=torch.float64, device="cuda")
+          for n, cnt, w in (("pd", v, K), ("vn", e, K), ("wn", v, K + 1), ("rho", v, K), ("signs", v, 6),
+                            ("dual", v, 1), ("flux", e, K), ("fluz", v, K + 1), ("div", v, K), ("out", v, K))}
+    fl["rho"] += 0.5
+    t3 = timed(lambda: _lib.call("tsg_transport_indirect", _lib.ptr(e2v), _lib.ptr(v2e), _lib.ptr(fl["signs"]),
+                                 _lib.ptr(fl["dual"]), _lib.ptr(fl["pd"]), _lib.ptr(fl["vn"]), _lib.ptr(fl["wn"]),
+                                 _lib.ptr(fl["rho"]), v, e, K, 0.1, 1.0, 0, _lib.ptr(fl["flux"]),
+                                 _lib.ptr(fl["fluz"]), _lib.ptr(fl["div"]), _lib.ptr(fl["out"]), s()))
+    # materialised flux / fluz / div: the unfused DISTINCT bytes plus the div output
+    record("mpdata_indirect", t3, unfused_bytes + 8 * v * K, patch=[rows, cols, K], updates_per_s=v * K / t3)
 
 
 if __name__ == "__main__":
