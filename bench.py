@@ -338,7 +338,8 @@ def run_ours(args):
                    "rows_per_gpu": my_rows, "vertices": GV, "edges": 3 * GV,
                    "dt": DT, "pivbz": PIVBZ, "parallelism": f"row-strips x{world}",
                    "halo_exchange": ("none" if world == 1 else
-                                     "fused P2P stores from the step epilogue (CUDA IPC over NVLink)"
+                                     "one launch per step: boundary-row epilogue stores into the "
+                                     "neighbours' halos (CUDA IPC over NVLink), in-kernel step fence"
                                      if args.exchange == "p2p" else "NCCL grouped send/recv"),
                    "l2": "256 MiB read-only L2 flush before every timed step (outside the events)",
                    "fused_tile": {"ti": vi[0].value, "tj": vi[1].value, "kc": vi[2].value,
@@ -355,7 +356,7 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "e2e_all_inputs": e2e_all,
-        "gpu_launches": args.steps * (1 if world == 1 else 3),
+        "gpu_launches": args.steps * (1 if world == 1 or args.exchange == "p2p" else 3),
         "clocks": clocks.summary(),
         "timed_wall_s": t_wall,
     }

@@ -125,6 +125,21 @@ int tsg_mpdata_step_rows_peer(tsg_grid *g, const double *pd, const double *vn, c
                               const double *rho, const double *signs, const double *dual,
                               double *pd_out, double dt, double pivbz, int flux_op, int row_lo,
                               int row_hi, double *halo_up, double *halo_down, tsg_stream s);
+/* One whole row-strip step in ONE launch, halo exchange and step fence included: the
+ * tile rows touching the strip's first / last row run last; before loading them the
+ * kernel acquires `my_flags[0..1] >= step` (both ring neighbours finished step-1, so its
+ * halo rows are complete and their pd_out halo rows are free), their epilogue stores the
+ * boundary rows into `halo_up` / `halo_down` as tsg_mpdata_step_rows_peer does, and the
+ * last CTA to finish (counted in the caller's zero-initialised `done_counter`, reset by
+ * the kernel) releases step+1 into `flag_up` (the up neighbour's flag word 1) and
+ * `flag_down` (the down neighbour's word 0).  A neighbour missing for `timeout_ms` sets
+ * `*error_word` instead of hanging.  Grid flags must not include TSG_PERIODIC_ROWS. */
+int tsg_mpdata_step_strip(tsg_grid *g, const double *pd, const double *vn, const double *wn,
+                          const double *rho, const double *signs, const double *dual,
+                          double *pd_out, double dt, double pivbz, int flux_op, double *halo_up,
+                          double *halo_down, const int64_t *my_flags, int64_t *flag_up,
+                          int64_t *flag_down, int64_t step, int timeout_ms, int *error_word,
+                          int *done_counter, tsg_stream s);
 /* The reference's time loop (bench.py:398-403: step, copy pd_out -> pd_in, repeat) as a
  * device ping-pong: step t reads pd_a and writes pd_b when t is even, the reverse when
  * odd, so after nsteps the newest density is in pd_b (nsteps odd) or pd_a (even) and the

@@ -74,10 +74,47 @@ struct FusedArgs {
     // fused halo exchange: the ring neighbours' halo rows (peer / IPC-mapped memory) that
     // receive this strip's first / last row; NULL = not exchanged by this kernel
     double *halo_up, *halo_down;
+    // single-launch strip step (tsg_mpdata_step_strip; PEER instantiation only): the tile
+    // rows touching the strip's first / last row run last (`rotate`), their producer
+    // first acquires my_flags >= wait_value (both neighbours finished the previous step),
+    // and the last CTA to finish releases wait_value + 1 into the neighbours' flag words
+    const int64_t *my_flags;
+    int64_t *flag_up, *flag_down;
+    int64_t wait_value;
+    uint64_t timeout_ns;
+    int *err, *done;
+    int rotate;
     double dt, pivbz;
-    int tiles_j, chunks;
+    int tiles_i, tiles_j, chunks;
     int64_t units;
 };
+
+__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
+    int64_t v;
+    asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// spin (with back-off) until both flag words reach `value`; on timeout report through `err`
+// and carry on, so a lost neighbour cannot hang the GPU
+__device__ inline void wait_both(const int64_t *flags, int64_t value, uint64_t timeout_ns, int *err) {
+    const uint64_t t0 = globaltimer_ns();
+    unsigned backoff = 32;
+    while (ld_acquire_sys(flags) < value || ld_acquire_sys(flags + 1) < value) {
+        if (globaltimer_ns() - t0 > timeout_ns) {
+            if (err) atomicExch(err, 1);
+            return;
+        }
+        __nanosleep(backoff);
+        if (backoff < 4096) backoff *= 2;
+    }
+}
 
 // LP: levels per thread.  LP = 1: thread per (vertex, level), LV lanes per vertex.
 // LP = 2: a thread owns the adjacent level pair (k, k+1): 16-byte shared loads and stores,
@@ -129,11 +166,23 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
     }
     __syncthreads();
 
+    // sequence tile row -> tile row: with `rotate` the boundary tile rows come last
+    // (order 1, 2, ..., T-1, 0) so only the final units wait for the neighbours
+    auto tile_row = [&](int t) { return (PEER && a.rotate) ? (t + 1 == a.tiles_i ? 0 : t + 1) : t; };
+    bool waited = !(PEER && a.my_flags);
+
     // producer cursor (thread 0 only), decoded once, then advanced incrementally
     int p_chunk = u_begin % a.chunks, p_tile = u_begin / a.chunks;
     int p_ti = p_tile / a.tiles_j, p_tj = p_tile % a.tiles_j;
     auto issue_next = [&](int stage) {
-        const int i0 = a.row_lo + p_ti * TI, j0 = p_tj * TJ, k0 = p_chunk * KC;
+        const int tr = tile_row(p_ti);
+        if constexpr (PEER) {
+            if (!waited && (tr == 0 || tr == a.tiles_i - 1)) {  // reads the neighbours' rows
+                wait_both(a.my_flags, a.wait_value, a.timeout_ns, a.err);
+                waited = true;
+            }
+        }
+        const int i0 = a.row_lo + tr * TI, j0 = p_tj * TJ, k0 = p_chunk * KC;
         unsigned char *base = smem + stage * C::kStageBytes;
         uint64_t *bar = &bars[stage];
         mbar_expect_tx(bar, C::kTxBytes);
@@ -176,7 +225,7 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
             if (OP != kComputeProbe) issue_next((n + STAGES - 1) % STAGES);
         }
         if (n == 0 || chunk == 0) {
-            const int i = a.row_lo + ti * TI + li, j = tj * TJ + lj;
+            const int i = a.row_lo + tile_row(ti) * TI + li, j = tj * TJ + lj;
             vvalid = i < a.row_hi && j < a.cols;
             if (vvalid) {
                 const int64_t cell = (int64_t)(i + 1) * (a.cols + 2) + (j + 1);
@@ -347,6 +396,18 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
             }
         }
         __syncthreads();  // every thread is done with this stage
+    }
+    if constexpr (PEER) {
+        if (a.done && tid == 0) {  // the last CTA out releases the step into both neighbours
+            __threadfence_system();  // this CTA's peer stores are visible system-wide
+            if (atomicAdd(a.done, 1) == (int)gridDim.x - 1) {
+                *a.done = 0;  // ready for the next launch (every CTA has arrived)
+                __threadfence_system();
+                const int64_t v = a.wait_value + 1;
+                if (a.flag_up) asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(a.flag_up), "l"(v) : "memory");
+                if (a.flag_down) asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(a.flag_down), "l"(v) : "memory");
+            }
+        }
     }
 }
 
@@ -529,11 +590,18 @@ static int prepare(tsg_grid *g, const double *pd, const double *vn, const double
     a.row_hi = row_hi;
     a.halo_up = halo_up;
     a.halo_down = halo_down;
+    a.my_flags = nullptr;
+    a.flag_up = a.flag_down = nullptr;
+    a.wait_value = 0;
+    a.timeout_ns = 0;
+    a.err = a.done = nullptr;
+    a.rotate = 0;
     a.K = K;
     a.flags = g->flags;
     a.dt = dt;
     a.pivbz = pivbz;
     const int tiles_i = (row_hi - row_lo + v.ti - 1) / v.ti;
+    a.tiles_i = tiles_i;
     a.tiles_j = (cols + v.tj - 1) / v.tj;
     a.chunks = (K + v.kc - 1) / v.kc;
     a.units = (int64_t)tiles_i * a.tiles_j * a.chunks;
@@ -574,6 +642,33 @@ extern "C" int tsg_mpdata_step_rows_peer(tsg_grid *g, const double *pd, const do
     if (int rc = prepare(g, pd, vn, wn, rho, signs, dual, pd_out, dt, pivbz, flux_op, row_lo,
                          row_hi, halo_up, halo_down, &L))
         return rc;
+    return launch(&L, s);
+}
+
+extern "C" int tsg_mpdata_step_strip(tsg_grid *g, const double *pd, const double *vn,
+                                     const double *wn, const double *rho, const double *signs,
+                                     const double *dual, double *pd_out, double dt, double pivbz,
+                                     int flux_op, double *halo_up, double *halo_down,
+                                     const int64_t *my_flags, int64_t *flag_up,
+                                     int64_t *flag_down, int64_t step, int timeout_ms,
+                                     int *error_word, int *done_counter, tsg_stream s) {
+    if (!g) return fail(TSG_EVALUE, "grid is NULL");
+    if (!my_flags || !done_counter) return fail(TSG_EVALUE, "tsg_mpdata_step_strip: NULL flags / counter");
+    if (step < 0 || timeout_ms < 0) return fail(TSG_EVALUE, "tsg_mpdata_step_strip: bad step / timeout");
+    if (!halo_up && !halo_down) return fail(TSG_EVALUE, "tsg_mpdata_step_strip: no neighbour halo rows");
+    FusedLaunch L;
+    if (int rc = prepare(g, pd, vn, wn, rho, signs, dual, pd_out, dt, pivbz, flux_op, 0, g->rows,
+                         halo_up, halo_down, &L))
+        return rc;
+    FusedArgs &a = L.a;
+    a.my_flags = my_flags;
+    a.flag_up = flag_up;
+    a.flag_down = flag_down;
+    a.wait_value = step;
+    a.timeout_ns = (uint64_t)timeout_ms * 1000000ull;
+    a.err = error_word;
+    a.done = done_counter;
+    a.rotate = 1;
     return launch(&L, s);
 }
 

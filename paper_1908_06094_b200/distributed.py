@@ -142,7 +142,7 @@ class StripStepper:
 
     def __init__(self, global_rows: int, cols: int, levels: int, rank: int, world: int,
                  seed: int = 0, group=None, flux_op: str = "upwind", exchange=None,
-                 mode: str = "nccl", timeout_ms: int = 20000):
+                 mode: str = "nccl", timeout_ms: int = 20000, single_launch: bool = True):
         self.strips = RowStrips(global_rows, world)
         self.rank, self.world, self.group = rank, world, group
         self.row0, self.nrows = self.strips.strip(rank)
@@ -155,6 +155,9 @@ class StripStepper:
             raise ValueError(f"exchange mode must be 'nccl' or 'p2p', got {mode!r}")
         self.mode = mode if world > 1 else "nccl"
         self.timeout_ms = timeout_ms
+        # p2p: the whole step in one launch (default) or the five-launch sequence
+        # (interior rows, fence, two boundary-row launches, signal)
+        self.single_launch = single_launch
         self.steps_done = 0
         if self.mode == "p2p":
             # the density buffers are whole cudaMalloc allocations so they can be IPC-exported
@@ -178,6 +181,7 @@ class StripStepper:
 
         self._flags = RawBuffer((2,), dtype="<i8")
         self._err = RawBuffer((1,), dtype="<i4")
+        self._done = RawBuffer((1,), dtype="<i4")  # CTA arrival counter of the strip launch
         mine = (self._raw[0].ipc_handle(), self._raw[1].ipc_handle(), self._flags.ipc_handle(),
                 self.nrows)
         every = [None] * self.world
@@ -255,10 +259,22 @@ class StripStepper:
             self.pending = self.exchange(self.pd_out, self.nrows, self.rank, self.world, self.group)
 
     def _step_p2p(self, dt: float, pivbz: float, main) -> None:
-        """Fused exchange: the boundary rows' epilogue stores into the neighbours' halos."""
+        """The whole strip step in one launch (tsg_mpdata_step_strip): interior tiles first,
+        then the boundary tile rows after an in-kernel acquire of the neighbours' step flags;
+        their epilogue stores into the neighbours' halos and the last CTA releases the step."""
         import ctypes
 
         n, s = self.steps_done, _lib.stream_handle(main)
+        if self.single_launch:
+            hu, hd = self._peer_rows()
+            up, down = self._peers[self.strips.up(self.rank)], self._peers[self.strips.down(self.rank)]
+            _lib.call("tsg_mpdata_step_strip", self.grid.handle, _lib.ptr(self.pd), _lib.ptr(self.vn),
+                      _lib.ptr(self.wn), _lib.ptr(self.rho), _lib.ptr(self.signs), _lib.ptr(self.dual),
+                      _lib.ptr(self.pd_out), float(dt), float(pivbz), self.flux_code, hu, hd,
+                      ctypes.c_void_p(self._flags.ptr), ctypes.c_void_p(up["flags"].ptr + 8),
+                      ctypes.c_void_p(down["flags"].ptr), n, self.timeout_ms,
+                      ctypes.c_void_p(self._err.ptr), ctypes.c_void_p(self._done.ptr), s)
+            return
         self._launch(1, self.nrows - 1, dt, pivbz, main)  # interior: no halo, no peers
         # neighbours finished step n-1: my halo rows are complete and their pd_out is free
         _lib.call("tsg_wait_flags", ctypes.c_void_p(self._flags.ptr), n, self.timeout_ms,

@@ -131,7 +131,7 @@ def test_strip_steppers_on_one_gpu_match_single_patch(cuda_ok):
     assert torch.equal(got, single.interior("pd"))
 
 
-def _p2p_worker(rank, world, port, q):
+def _p2p_worker(rank, world, port, q, single_launch=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -139,7 +139,8 @@ def _p2p_worker(rank, world, port, q):
         from paper_1908_06094_b200.distributed import StripStepper
 
         rows, cols, K = 17, 29, 18
-        st = StripStepper(rows, cols, K, rank, world, seed=7, mode="p2p", timeout_ms=60000)
+        st = StripStepper(rows, cols, K, rank, world, seed=7, mode="p2p", timeout_ms=60000,
+                          single_launch=single_launch)
         for _ in range(4):
             st.step(0.2, 0.8)
             st.swap()
@@ -164,17 +165,20 @@ def _p2p_worker(rank, world, port, q):
 
 
 @pytest.mark.gpu
-def test_p2p_fused_exchange_processes_share_one_gpu(cuda_ok):
-    """Two ranks (processes) on one GPU: IPC-mapped density buffers, boundary rows stored
+@pytest.mark.parametrize("world,single_launch", [(2, True), (2, False), (3, True)])
+def test_p2p_fused_exchange_processes_share_one_gpu(cuda_ok, world, single_launch):
+    """Ranks (processes) on one GPU: IPC-mapped density buffers, boundary rows stored
     straight into the neighbour's halo by the step kernel, device-side step fence -- the
-    multi-GPU fused-exchange path end to end; result == single-patch step bitwise."""
+    multi-GPU fused-exchange path end to end, as one launch per step (in-kernel fence and
+    release) or as the five-launch sequence; result == single-patch step bitwise."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_p2p_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, q, single_launch))
+             for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=300) for _ in range(2)]
+    res = [q.get(timeout=300) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
     assert all(p.exitcode == 0 for p in procs)
