@@ -317,7 +317,8 @@ def run_ours(args):
     import ctypes
 
     vi = [ctypes.c_int() for _ in range(6)]
-    _l().tsg_fused_variant_info(0, *[ctypes.byref(x) for x in vi])
+    variant = _l().tsg_fused_variant_of(stepper.grid.handle, 0, my_rows)
+    _l().tsg_fused_variant_info(variant, *[ctypes.byref(x) for x in vi])
     cpu = None
     if not args.no_cpu:
         cr = w["cpu_rows"]
@@ -342,7 +343,7 @@ def run_ours(args):
                                      "neighbours' halos (CUDA IPC over NVLink), in-kernel step fence"
                                      if args.exchange == "p2p" else "NCCL grouped send/recv"),
                    "l2": "256 MiB read-only L2 flush before every timed step (outside the events)",
-                   "fused_tile": {"ti": vi[0].value, "tj": vi[1].value, "kc": vi[2].value,
+                   "fused_tile": {"variant": variant, "ti": vi[0].value, "tj": vi[1].value, "kc": vi[2].value,
                                   "stages": vi[3].value, "threads": vi[4].value,
                                   "smem_bytes": vi[5].value}},
         "effective_gbs": achieved,

@@ -163,10 +163,15 @@ int tsg_transport_indirect(const int64_t *e2v, const int64_t *v2e, const double 
                            const double *wn, const double *rho, int64_t nv, int64_t ne,
                            int nlev, double dt, double pivbz, int flux_op, double *flux,
                            double *fluz, double *div, double *pd_out, tsg_stream s);
-/* Select the fused kernel's tile variant (0 = default); variant 0 in _info = current. */
+/* Select the fused kernel's tile variant; 0 (the default) chooses per launch: the compact
+ * 4x16 tile when the tile above a tile is still in L2 under the contiguous schedule, else
+ * the tall 16x4 tile (tsg_fused_variant_of).  Variant 0 in _info = the forced variant, or
+ * the compact tile when none is forced. */
 int tsg_set_fused_variant(int variant);
 int tsg_fused_variant_info(int variant, int *ti, int *tj, int *kc, int *stages, int *threads,
                            int *smem_bytes);
+/* The variant a fused launch over logical rows [row_lo, row_hi) of `g` uses (-1 on error). */
+int tsg_fused_variant_of(const tsg_grid *g, int row_lo, int row_hi);
 
 /* ---- neighbour reductions (stencil.py:401-408; kernels.py:27-104; reference.py:137-157) */
 /* Structured ("direct") reduce for any of the 9 relations (connectivity.py:36-68):

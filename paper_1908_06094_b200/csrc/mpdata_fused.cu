@@ -459,13 +459,35 @@ static Variant *variants(int *count) {
         make_variant<4, 8, 16, 3, 8, 2>(),   // 16: level pairs, 256 threads, 2 CTAs / SM
         make_variant<2, 16, 16, 2, 8, 2>(),  // 17: level pairs, 256 threads, 2 CTAs / SM
         make_variant<8, 8, 16, 3, 8, 2>(),   // 18: level pairs, 512 threads, 3 x 63 KB
+        make_variant<16, 4, 16, 3, 8, 2>(),  // 19: level pairs, 512 threads, tall tiles
+        make_variant<32, 2, 16, 3, 8, 2>(),  // 20: level pairs, 512 threads, taller tiles
     };
     *count = (int)(sizeof(v) / sizeof(v[0]));
     return v;
 }
 
-static constexpr int kDefaultVariant = 15;
-static int g_variant = kDefaultVariant;
+// Default tile choice (g_variant == 0).  Units run in contiguous per-CTA ranges of the
+// tile-major order, so the tile above a tile -- whose last rows are this tile's upper pd
+// and vn halo -- was loaded R = tiles_j * chunks units of the order earlier.  When that
+// load is still in L2 (it happened at most kReuseUnits units earlier in the CTA running
+// it; every unit of the whole grid moves ~10 MB through L2 meanwhile), the compact 4x16
+// tile is best (279x256x80: 63.6 vs 65.5 us for 16x4).  Otherwise every upper halo is
+// re-read from DRAM (ncu at O1280: 32 % of the step's reads) and the tall 16x4 tile, with
+// two halo rows per 16 instead of per 4, is faster (O1280: 10.06-10.12 vs 10.41-10.47 ms).
+static constexpr int kCompactVariant = 15, kTallVariant = 19;
+constexpr double kReuseUnits = 8.0;
+static int g_variant = 0;  // 0 = choose per launch (pick_variant)
+
+static int pick_variant(const tsg_grid *g, int nrows) {
+    if (g_variant) return g_variant;
+    int n = 0;
+    const Variant &v = variants(&n)[kCompactVariant - 1];
+    const double tiles_j = (g->cols + v.tj - 1) / v.tj, chunks = (g->levels + v.kc - 1) / v.kc;
+    const double units = (double)((nrows + v.ti - 1) / v.ti) * tiles_j * chunks;
+    const double range = units / g->num_sms, R = tiles_j * chunks;
+    const double gap = R < range ? R : R - range * (double)(int64_t)(R / range);
+    return gap <= kReuseUnits ? kCompactVariant : kTallVariant;
+}
 
 }  // namespace tsg
 
@@ -475,7 +497,7 @@ extern "C" int tsg_set_fused_variant(int variant) {
     int n = 0;
     variants(&n);
     if (variant < 0 || variant > n) return fail(TSG_EVALUE, "fused variant must be in [0, %d]", n);
-    g_variant = variant == 0 ? kDefaultVariant : variant;
+    g_variant = variant;  // 0: the per-launch default (pick_variant)
     return TSG_OK;
 }
 
@@ -483,7 +505,7 @@ extern "C" int tsg_fused_variant_info(int variant, int *ti, int *tj, int *kc, in
                                       int *threads, int *smem_bytes) {
     int n = 0;
     Variant *vs = variants(&n);
-    if (variant == 0) variant = g_variant;
+    if (variant == 0) variant = g_variant ? g_variant : kCompactVariant;
     if (variant < 1 || variant > n) return fail(TSG_EVALUE, "fused variant must be in [1, %d]", n);
     const Variant &v = vs[variant - 1];
     if (ti) *ti = v.ti;
@@ -493,6 +515,18 @@ extern "C" int tsg_fused_variant_info(int variant, int *ti, int *tj, int *kc, in
     if (threads) *threads = v.threads;
     if (smem_bytes) *smem_bytes = v.smem;
     return TSG_OK;
+}
+
+extern "C" int tsg_fused_variant_of(const tsg_grid *g, int row_lo, int row_hi) {
+    if (!g) {
+        fail(TSG_EVALUE, "grid is NULL");
+        return -1;
+    }
+    if (row_lo < 0 || row_hi > g->rows || row_lo > row_hi) {
+        fail(TSG_EVALUE, "row range [%d, %d) outside [0, %d)", row_lo, row_hi, g->rows);
+        return -1;
+    }
+    return pick_variant(g, row_hi - row_lo);
 }
 
 extern "C" int tsg_mpdata_step(tsg_grid *g, const double *pd, const double *vn, const double *wn,
@@ -555,7 +589,8 @@ static int prepare(tsg_grid *g, const double *pd, const double *vn, const double
 
     int n = 0;
     Variant *vs = variants(&n);
-    const Variant &v = vs[g_variant - 1];
+    const int vi = pick_variant(g, row_hi - row_lo);
+    const Variant &v = vs[vi - 1];
 
     const int rows = g->rows, cols = g->cols;
     const cuuint64_t pv = (cuuint64_t)pitch_of(K), pw = (cuuint64_t)pitch_of(K + 1);
@@ -615,7 +650,7 @@ static int prepare(tsg_grid *g, const double *pd, const double *vn, const double
     TSG_CHECK_CUDA(cudaFuncSetAttribute(L->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
     int per_sm = 0;
     TSG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L->fn, v.threads, v.smem));
-    if (per_sm < 1) return fail(TSG_ECUDA, "fused variant %d does not fit on an SM", g_variant);
+    if (per_sm < 1) return fail(TSG_ECUDA, "fused variant %d does not fit on an SM", vi);
     int64_t grid = (int64_t)g->num_sms * per_sm;
     if (grid > a.units) grid = a.units;
     L->grid = (int)grid;
@@ -689,7 +724,7 @@ extern "C" int tsg_mpdata_run(tsg_grid *g, double *pd_a, double *pd_b, const dou
     bwd.a.pd_out = pd_a;
     {
         int n = 0;
-        if (int rc = encode_pd(variants(&n)[g_variant - 1], g, pd_b, &bwd.m_pd)) return rc;
+        if (int rc = encode_pd(variants(&n)[pick_variant(g, g->rows) - 1], g, pd_b, &bwd.m_pd)) return rc;
     }
     for (int t = 0; t < nsteps; ++t)
         if (int rc = launch(t % 2 == 0 ? &fwd : &bwd, s)) return rc;

@@ -316,6 +316,24 @@ def test_extreme_dual_volumes(cuda_ok):
     assert np.array_equal(got, want, equal_nan=True)
 
 
+def test_default_fused_variant_follows_the_l2_reuse_rule(cuda_ok):
+    """Variant 0 picks the compact 4x16 tile when the tile above is still in L2 under the
+    contiguous schedule (the bench patch) and the tall 16x4 tile otherwise (O1280-class)."""
+    from paper_1908_06094_b200 import _lib
+    from paper_1908_06094_b200.device import DeviceGrid
+
+    lib = _lib.lib()
+    bench, big = DeviceGrid(279, 256, 80), DeviceGrid(2560, 2576, 137)
+    assert lib.tsg_fused_variant_of(bench.handle, 0, 279) == 15
+    assert lib.tsg_fused_variant_of(big.handle, 0, 2560) == 19
+    _lib.call("tsg_set_fused_variant", 18)
+    try:
+        assert lib.tsg_fused_variant_of(bench.handle, 0, 279) == 18
+    finally:
+        _lib.call("tsg_set_fused_variant", 0)
+    assert lib.tsg_fused_variant_of(bench.handle, 5, 400) == -1
+
+
 def test_every_fused_variant_is_bitwise_identical(cuda_ok):
     from paper_1908_06094_b200 import _lib
     from tests.gpu_helpers import fused_step

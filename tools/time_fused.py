@@ -6,7 +6,7 @@ from paper_1908_06094_b200 import PatchSpec, StructuredStepper, _lib
 from paper_1908_06094_b200.workloads import transport_inputs, mpdata_algorithmic_bytes
 
 op = int(sys.argv[1]) if len(sys.argv) > 1 else 0
-variants = [int(v) for v in sys.argv[2:]] or [1]
+variants = [int(v) for v in sys.argv[2:]] or [0]
 shape = (279, 256, 80)
 inp = transport_inputs(*shape)
 st = StructuredStepper(PatchSpec(*shape))
