@@ -20,11 +20,15 @@ __host__ __device__ constexpr int red_ti(int ct) { return ct == 1 ? 4 : 8; }
 
 constexpr int kRedLanes = kRedKC / 2;  // threads per element: one level pair each
 
-template <int CT>
+// TALL: the tile transposed (16 rows x red_ti columns) -- two halo rows per 16 instead of
+// per 4 or 8, for patches whose tile above is no longer in L2 when a tile is loaded
+// (launch_reduce_tma; the fused kernel's rule, mpdata_fused.cu pick_variant)
+template <int CT, bool TALL = false>
 struct RedCfg {
-    static constexpr int TI = red_ti(CT);
-    static constexpr int kThreads = TI * kRedTJ * kRedLanes;
-    static constexpr int kBoxBytes = (TI + 2) * CT * (kRedTJ + 2) * kRedKC * 8;
+    static constexpr int TI = TALL ? kRedTJ : red_ti(CT);
+    static constexpr int TJ = TALL ? red_ti(CT) : kRedTJ;
+    static constexpr int kThreads = TI * TJ * kRedLanes;
+    static constexpr int kBoxBytes = (TI + 2) * CT * (TJ + 2) * kRedKC * 8;
     static constexpr int kStageBytes = (kBoxBytes + 127) / 128 * 128;
     static constexpr int kSmemBytes = kRedStages * kStageBytes + 128;
 };
@@ -41,12 +45,12 @@ struct RedArgs {
 // MODE 0: sum fold (times scale[from] if SCALE); MODE 1: cell divergence
 // sum vn*length / area; MODE 2: weighted cell divergence sum vn*weights[c, n]
 // (mpdata.py:361-376; reference.py:119-134)
-template <int REL, bool SCALE, int MODE = 0>
+template <int REL, bool SCALE, int MODE = 0, bool TALL = false>
 __global__ void __launch_bounds__(red_ti(loc_colors(REL % 3)) * kRedTJ * kRedLanes)
     reduce_tma_kernel(const __grid_constant__ CUtensorMap tm_src, const RedArgs a) {
     constexpr int CF = loc_colors(REL / 3), CT = loc_colors(REL % 3), W = rel_width(REL);
-    constexpr int TI = red_ti(CT), TJ = kRedTJ, KC = kRedKC, STAGES = kRedStages;
-    using C = RedCfg<CT>;
+    using C = RedCfg<CT, TALL>;
+    constexpr int TI = C::TI, TJ = C::TJ, KC = kRedKC, STAGES = kRedStages;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * C::kStageBytes);
 
@@ -183,17 +187,16 @@ __global__ void __launch_bounds__(red_ti(loc_colors(REL % 3)) * kRedTJ * kRedLan
     }
 }
 
-template <int REL, bool SCALE, int MODE = 0>
-static int launch_reduce_tma(const tsg_grid *g, int inner, const double *src, const double *scale,
-                             double *dst, cudaStream_t st, const double *length = nullptr,
-                             const double *area = nullptr, const double *weights = nullptr) {
+template <int REL, bool SCALE, int MODE, bool TALL>
+static int launch_reduce_shape(const tsg_grid *g, int inner, const double *src, const double *scale,
+                               double *dst, cudaStream_t st, const double *length,
+                               const double *area, const double *weights) {
     constexpr int CT = loc_colors(REL % 3);
-    using C = RedCfg<CT>;
-    if (int rc = get_encode()) return rc;
+    using C = RedCfg<CT, TALL>;
     const cuuint64_t p = (cuuint64_t)pitch_of(inner), W = (cuuint64_t)g->cols + 2, H = (cuuint64_t)g->rows + 2;
     cuuint64_t dims[4] = {(cuuint64_t)inner, W, (cuuint64_t)CT, H};
     cuuint64_t str[3] = {p * 8, W * p * 8, CT * W * p * 8};
-    cuuint32_t box[4] = {kRedKC, kRedTJ + 2, (cuuint32_t)CT, (cuuint32_t)C::TI + 2};
+    cuuint32_t box[4] = {kRedKC, (cuuint32_t)C::TJ + 2, (cuuint32_t)CT, (cuuint32_t)C::TI + 2};
     CUtensorMap m;
     if (int rc = make_map(&m, src, 4, dims, str, box)) return rc;
     RedArgs a;
@@ -206,11 +209,11 @@ static int launch_reduce_tma(const tsg_grid *g, int inner, const double *src, co
     a.cols = g->cols;
     a.nk = inner;
     a.flags = g->flags;
-    a.tiles_j = (g->cols + kRedTJ - 1) / kRedTJ;
+    a.tiles_j = (g->cols + C::TJ - 1) / C::TJ;
     a.chunks = (inner + kRedKC - 1) / kRedKC;
     a.units = (int64_t)((g->rows + C::TI - 1) / C::TI) * a.tiles_j * a.chunks;
     if (a.units >= (1LL << 31)) return fail(TSG_EVALUE, "field too large for one reduce launch");
-    void *fn = (void *)reduce_tma_kernel<REL, SCALE, MODE>;
+    void *fn = (void *)reduce_tma_kernel<REL, SCALE, MODE, TALL>;
     TSG_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
     int per_sm = 0;
     TSG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, C::kThreads, C::kSmemBytes));
@@ -219,6 +222,33 @@ static int launch_reduce_tma(const tsg_grid *g, int inner, const double *src, co
     void *args[] = {&m, &a};
     TSG_CHECK_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(C::kThreads), args, C::kSmemBytes, st));
     return TSG_OK;
+}
+
+// The compact tile unless the tile above a tile (its upper halo) was loaded more than
+// kRedReuseUnits units earlier in the contiguous per-CTA schedule (then evicted from L2).
+constexpr double kRedReuseUnits = 8.0;
+
+template <int REL, bool SCALE, int MODE = 0>
+static int launch_reduce_tma(const tsg_grid *g, int inner, const double *src, const double *scale,
+                             double *dst, cudaStream_t st, const double *length = nullptr,
+                             const double *area = nullptr, const double *weights = nullptr) {
+    constexpr int CT = loc_colors(REL % 3);
+    using C = RedCfg<CT, false>;
+    if (int rc = get_encode()) return rc;
+    static int per_sm = 0;  // resident compact CTAs per SM (same for every call)
+    if (!per_sm) {
+        void *fn = (void *)reduce_tma_kernel<REL, SCALE, MODE, false>;
+        TSG_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
+        TSG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, C::kThreads, C::kSmemBytes));
+        if (per_sm < 1) per_sm = 1;
+    }
+    const double tiles_j = (g->cols + C::TJ - 1) / C::TJ, chunks = (inner + kRedKC - 1) / kRedKC;
+    const double units = (double)((g->rows + C::TI - 1) / C::TI) * tiles_j * chunks;
+    const double range = units / ((double)g->num_sms * per_sm), R = tiles_j * chunks;
+    const double gap = R < range ? R : R - range * (double)(int64_t)(R / range);
+    if (gap <= kRedReuseUnits)
+        return launch_reduce_shape<REL, SCALE, MODE, false>(g, inner, src, scale, dst, st, length, area, weights);
+    return launch_reduce_shape<REL, SCALE, MODE, true>(g, inner, src, scale, dst, st, length, area, weights);
 }
 
 // dispatch over the nine relations; returns TSG_OK or an error
