@@ -260,7 +260,8 @@ def test_device_halo_update_matches_host(cuda_ok):
     assert np.array_equal(f.array()[0], f.array()[r])
 
 
-@pytest.mark.parametrize("shape", [(6, 5, 2), (6, 5, 137), (2, 2, 3), (11, 3, 17), (4, 70, 81)])
+@pytest.mark.parametrize("shape", [(6, 5, 2), (6, 5, 137), (2, 2, 3), (11, 3, 17), (4, 70, 81),
+                                   (5, 9, 63), (7, 6, 64), (3, 17, 65)])  # the pitch-16 threshold
 def test_edge_shapes_fused_unfused_indirect(cuda_ok, shape):
     from tests.gpu_helpers import fused_step, oracle_tables, unfused_step
 
@@ -285,6 +286,7 @@ def test_nan_and_signed_zero_semantics(cuda_ok):
     r, c, lev = 6, 7, 5
     inp = O.transport_inputs(r, c, lev, 2, "random", "random", "random")
     inp["vn"][3, 2] = np.nan
+    inp["vn"][5, 1] = -np.nan  # sign-bit-set NaN
     inp["vn"][10, 1] = -0.0
     inp["vn"][11, :] = 0.0
     inp["wn"][4, 2] = np.nan
@@ -294,11 +296,15 @@ def test_nan_and_signed_zero_semantics(cuda_ok):
     got = fused_step(r, c, lev, inp, 0.2, 0.8)
     assert np.array_equal(np.isnan(got), np.isnan(want["pd_out"]))
     assert np.array_equal(got, want["pd_out"], equal_nan=True)
-    assert np.array_equal(np.signbit(got), np.signbit(want["pd_out"]))
+    # zero signs must match; a NaN's sign / payload is not part of the contract (the GPU
+    # returns the canonical NaN, numpy propagates an input's)
+    real = ~np.isnan(want["pd_out"])
+    assert np.array_equal(np.signbit(got[real]), np.signbit(want["pd_out"][real]))
     un = unfused_step(r, c, lev, inp, 0.2, 0.8)
     for k in want:
         assert np.array_equal(un[k], want[k], equal_nan=True), k
-        assert np.array_equal(np.signbit(un[k]), np.signbit(want[k])), k
+        real = ~np.isnan(want[k])
+        assert np.array_equal(np.signbit(un[k][real]), np.signbit(want[k][real])), k
 
 
 def test_extreme_dual_volumes(cuda_ok):
