@@ -301,6 +301,23 @@ def run_ours(args):
         e2e_all = e2e_run(pinned, "StructuredStepper.run_pipelined, the flat oracle call pattern "
                                   "(reference.py:93-116): H2D of pd / vn / wn / rho every step")
 
+    # back-to-back time loop (tsg_mpdata_run ping-pong, no L2 flush: the 320 MB of inputs
+    # exceed the 126 MB L2), the reference's bench loop (bench.py:398-403) -- informational
+    loop = None
+    if host_fed:
+        n_loop = 100
+        stepper.run(n_loop, DT, PIVBZ)
+        torch.cuda.synchronize()
+        l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0.record(stream)
+        stepper.run(n_loop, DT, PIVBZ)
+        l1.record(stream)
+        torch.cuda.synchronize()
+        t_loop = l0.elapsed_time(l1) / 1e3 / n_loop
+        loop = {"value": V * K / t_loop, "unit": UNIT, "ms_per_step": t_loop * 1e3, "steps": n_loop,
+                "l2": "no flush: inputs (320 MB) larger than L2",
+                "api": "StructuredStepper.run (tsg_mpdata_run, one fused launch per step)"}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -357,6 +374,7 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "e2e_all_inputs": e2e_all,
+        "time_loop": loop,
         "gpu_launches": args.steps * (1 if world == 1 or args.exchange == "p2p" else 3),
         "clocks": clocks.summary(),
         "timed_wall_s": t_wall,
