@@ -134,6 +134,8 @@ def cpu_reference_steps(steps: int, warmup: int, budget_s: float | None = None, 
     from oracle import c_oracle
     from oracle import tsg_oracle as O
 
+    # every host core this process may run on (torchrun exports OMP_NUM_THREADS=1 per rank)
+    c_oracle.set_threads(len(os.sched_getaffinity(0)))
     inp = O.transport_inputs(rows, cols, levels, 0, "uniform", "gaussian-bump", "one")
     e2v = O.neighbor_table(rows, cols, "edges", "vertices")
     v2e = O.neighbor_table(rows, cols, "vertices", "edges")
