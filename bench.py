@@ -339,7 +339,7 @@ def run_ours(args):
     variant = _l().tsg_fused_variant_of(stepper.grid.handle, 0, my_rows)
     _l().tsg_fused_variant_info(variant, *[ctypes.byref(x) for x in vi])
     cpu = None
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:  # the host baseline is measured at N = 1 only
         cr = w["cpu_rows"]
         times, threads = cpu_reference_steps(0, 1 if cr == w["rows"] else 0, budget_s=args.cpu_seconds,
                                              rows=cr, cols=cols, levels=K)
