@@ -138,13 +138,28 @@ int tsg_mpdata_step_strip(tsg_grid *g, const double *pd, const double *vn, const
                           const double *rho, const double *signs, const double *dual,
                           double *pd_out, double dt, double pivbz, int flux_op, double *halo_up,
                           double *halo_down, const int64_t *my_flags, int64_t *flag_up,
-                          int64_t *flag_down, int64_t step, int timeout_ms, int *error_word,
-                          int *done_counter, tsg_stream s);
+                          int64_t *flag_down, int64_t step, int64_t *epoch, int timeout_ms,
+                          int *error_word, int *done_counter, tsg_stream s);
+/* `epoch` (optional, device memory): when non-NULL the step number is read from it at
+ * the start of the launch and advanced by the launch's last CTA, so a loop of strip steps
+ * needs no per-step argument; `step` is then ignored.  tsg_mpdata_run_strip runs `nsteps`
+ * such steps ping-ponging pd_a / pd_b (halo_*_a: the neighbours' halo rows in their b
+ * buffer, written while stepping a -> b; halo_*_b likewise for b -> a) as a captured
+ * two-step CUDA graph (cached on the grid handle), halo exchange and fences included. */
+int tsg_mpdata_run_strip(tsg_grid *g, double *pd_a, double *pd_b, const double *vn,
+                         const double *wn, const double *rho, const double *signs,
+                         const double *dual, double dt, double pivbz, int flux_op,
+                         double *halo_up_a, double *halo_down_a, double *halo_up_b,
+                         double *halo_down_b, const int64_t *my_flags, int64_t *flag_up,
+                         int64_t *flag_down, int64_t *epoch, int timeout_ms, int *error_word,
+                         int *done_counter, int nsteps, tsg_stream s);
 /* The reference's time loop (bench.py:398-403: step, copy pd_out -> pd_in, repeat) as a
  * device ping-pong: step t reads pd_a and writes pd_b when t is even, the reverse when
  * odd, so after nsteps the newest density is in pd_b (nsteps odd) or pd_a (even) and the
  * other buffer holds the state before the last step.  vn / wn / rho / signs / dual are
- * fixed over the loop, as in the reference; the tensor maps are encoded once. */
+ * fixed over the loop, as in the reference; the tensor maps are encoded once, and from 4
+ * steps on the two alternating launches are replayed as a captured CUDA graph (cached on
+ * the grid handle until the arguments change). */
 int tsg_mpdata_run(tsg_grid *g, double *pd_a, double *pd_b, const double *vn, const double *wn,
                    const double *rho, const double *signs, const double *dual, double dt,
                    double pivbz, int flux_op, int nsteps, tsg_stream s);

@@ -39,7 +39,9 @@ SIGNATURES = {
     "tsg_mpdata_step_rows_peer": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _c_dbl, _c_dbl, _c_int,
                                            _c_int, _c_int, _p, _p, _p]),
     "tsg_mpdata_step_strip": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _c_dbl, _c_dbl, _c_int,
-                                       _p, _p, _p, _p, _p, _c_i64, _c_int, _p, _p, _p]),
+                                       _p, _p, _p, _p, _p, _c_i64, _p, _c_int, _p, _p, _p]),
+    "tsg_mpdata_run_strip": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _c_dbl, _c_dbl, _c_int,
+                                      _p, _p, _p, _p, _p, _p, _p, _p, _c_int, _p, _p, _c_int, _p]),
     "tsg_malloc": (_c_int, [_c_i64, ctypes.POINTER(_p)]),
     "tsg_free": (_c_int, [_p]),
     "tsg_ipc_handle": (_c_int, [_p, ctypes.c_char_p]),

@@ -30,6 +30,8 @@
 //    straight to HBM with one 16-byte store.  The LP = 1 variants (1-14) run one thread
 //    per (vertex, level) instead.
 //  * No tensor cores: fp64 stencil, ~0.5 flop/byte, the HBM roofline bounds it.
+#include <string.h>
+
 #include "tsg_tma.cuh"
 
 namespace tsg {
@@ -81,6 +83,8 @@ struct FusedArgs {
     const int64_t *my_flags;
     int64_t *flag_up, *flag_down;
     int64_t wait_value;
+    int64_t *epoch;  // non-NULL: the step counter lives here (read at start, advanced by
+                     // the last CTA) -- launches then take no per-step argument (CUDA graphs)
     uint64_t timeout_ns;
     int *err, *done;
     int rotate;
@@ -170,6 +174,10 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
     // (order 1, 2, ..., T-1, 0) so only the final units wait for the neighbours
     auto tile_row = [&](int t) { return (PEER && a.rotate) ? (t + 1 == a.tiles_i ? 0 : t + 1) : t; };
     bool waited = !(PEER && a.my_flags);
+    int64_t wv = a.wait_value;  // the step this launch performs
+    if constexpr (PEER) {
+        if (a.epoch) wv = *reinterpret_cast<volatile const int64_t *>(a.epoch);
+    }
 
     // producer cursor (thread 0 only), decoded once, then advanced incrementally
     int p_chunk = u_begin % a.chunks, p_tile = u_begin / a.chunks;
@@ -178,7 +186,7 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
         const int tr = tile_row(p_ti);
         if constexpr (PEER) {
             if (!waited && (tr == 0 || tr == a.tiles_i - 1)) {  // reads the neighbours' rows
-                wait_both(a.my_flags, a.wait_value, a.timeout_ns, a.err);
+                wait_both(a.my_flags, wv, a.timeout_ns, a.err);
                 waited = true;
             }
         }
@@ -402,8 +410,9 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
             __threadfence_system();  // this CTA's peer stores are visible system-wide
             if (atomicAdd(a.done, 1) == (int)gridDim.x - 1) {
                 *a.done = 0;  // ready for the next launch (every CTA has arrived)
+                if (a.epoch) *a.epoch = wv + 1;  // every CTA read it at its start
                 __threadfence_system();
-                const int64_t v = a.wait_value + 1;
+                const int64_t v = wv + 1;
                 if (a.flag_up) asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(a.flag_up), "l"(v) : "memory");
                 if (a.flag_down) asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(a.flag_down), "l"(v) : "memory");
             }
@@ -475,6 +484,7 @@ static Variant *variants(int *count) {
 // re-read from DRAM (ncu at O1280: 32 % of the step's reads) and the tall 16x4 tile, with
 // two halo rows per 16 instead of per 4, is faster (O1280: 10.06-10.12 vs 10.41-10.47 ms).
 static constexpr int kCompactVariant = 15, kTallVariant = 19;
+constexpr int kGraphMinSteps = 4;  // tsg_mpdata_run replays a captured two-step graph from here
 constexpr double kReuseUnits = 8.0;
 static int g_variant = 0;  // 0 = choose per launch (pick_variant)
 
@@ -628,6 +638,7 @@ static int prepare(tsg_grid *g, const double *pd, const double *vn, const double
     a.my_flags = nullptr;
     a.flag_up = a.flag_down = nullptr;
     a.wait_value = 0;
+    a.epoch = nullptr;
     a.timeout_ns = 0;
     a.err = a.done = nullptr;
     a.rotate = 0;
@@ -680,30 +691,97 @@ extern "C" int tsg_mpdata_step_rows_peer(tsg_grid *g, const double *pd, const do
     return launch(&L, s);
 }
 
+static int prepare_strip(tsg_grid *g, const double *pd, const double *vn, const double *wn,
+                         const double *rho, const double *signs, const double *dual, double *pd_out,
+                         double dt, double pivbz, int flux_op, double *halo_up, double *halo_down,
+                         const int64_t *my_flags, int64_t *flag_up, int64_t *flag_down, int64_t step,
+                         int64_t *epoch, int timeout_ms, int *error_word, int *done_counter,
+                         FusedLaunch *L) {
+    if (!g) return fail(TSG_EVALUE, "grid is NULL");
+    if (!my_flags || !done_counter) return fail(TSG_EVALUE, "tsg_mpdata_step_strip: NULL flags / counter");
+    if (step < 0 || timeout_ms < 0) return fail(TSG_EVALUE, "tsg_mpdata_step_strip: bad step / timeout");
+    if (!halo_up && !halo_down) return fail(TSG_EVALUE, "tsg_mpdata_step_strip: no neighbour halo rows");
+    if (int rc = prepare(g, pd, vn, wn, rho, signs, dual, pd_out, dt, pivbz, flux_op, 0, g->rows,
+                         halo_up, halo_down, L))
+        return rc;
+    FusedArgs &a = L->a;
+    a.my_flags = my_flags;
+    a.flag_up = flag_up;
+    a.flag_down = flag_down;
+    a.wait_value = step;
+    a.epoch = epoch;
+    a.timeout_ns = (uint64_t)timeout_ms * 1000000ull;
+    a.err = error_word;
+    a.done = done_counter;
+    a.rotate = 1;
+    return TSG_OK;
+}
+
+// ---- time loops as CUDA graphs ---------------------------------------------------------
+// A loop of steps alternates two launches (a -> b, b -> a) whose arguments do not change
+// from step to step (the strip steps keep their step counter on the device), so two steps
+// are captured once into a graph and replayed: one graph launch per two steps, no per-step
+// host work.  The executable graph is cached on the grid handle and rebuilt when the
+// arguments change.
+struct GraphCache {
+    FusedLaunch fwd, bwd;  // the captured pair (compared bytewise to detect a change)
+    cudaGraphExec_t exec;
+};
+
+void tsg::destroy_graph_cache(tsg_grid *g) {
+    if (!g->graph) return;
+    GraphCache *c = static_cast<GraphCache *>(g->graph);
+    cudaDeviceSynchronize();  // no launch of it may be in flight
+    cudaGraphExecDestroy(c->exec);
+    delete c;
+    g->graph = nullptr;
+}
+
+static int run_pair_graph(tsg_grid *g, const FusedLaunch &fwd, const FusedLaunch &bwd, int nsteps,
+                          tsg_stream s) {
+    GraphCache *c = static_cast<GraphCache *>(g->graph);
+    if (!c || memcmp(&c->fwd, &fwd, sizeof(fwd)) || memcmp(&c->bwd, &bwd, sizeof(bwd))) {
+        destroy_graph_cache(g);
+        cudaStream_t cap;
+        TSG_CHECK_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        c = new GraphCache;
+        c->fwd = fwd;
+        c->bwd = bwd;
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+        if (e == cudaSuccess) {
+            launch(&c->fwd, cap);
+            launch(&c->bwd, cap);
+            e = cudaStreamEndCapture(cap, &graph);
+        }
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&c->exec, graph, 0);
+        if (graph) cudaGraphDestroy(graph);
+        cudaStreamDestroy(cap);
+        if (e != cudaSuccess) {
+            delete c;
+            return fail(TSG_ECUDA, "time-loop graph capture failed: %s", cudaGetErrorString(e));
+        }
+        g->graph = c;
+    }
+    for (int t = 0; t + 1 < nsteps; t += 2)
+        TSG_CHECK_CUDA(cudaGraphLaunch(c->exec, (cudaStream_t)s));
+    if (nsteps % 2) return launch(&c->fwd, s);
+    return TSG_OK;
+}
+
 extern "C" int tsg_mpdata_step_strip(tsg_grid *g, const double *pd, const double *vn,
                                      const double *wn, const double *rho, const double *signs,
                                      const double *dual, double *pd_out, double dt, double pivbz,
                                      int flux_op, double *halo_up, double *halo_down,
                                      const int64_t *my_flags, int64_t *flag_up,
-                                     int64_t *flag_down, int64_t step, int timeout_ms,
-                                     int *error_word, int *done_counter, tsg_stream s) {
-    if (!g) return fail(TSG_EVALUE, "grid is NULL");
-    if (!my_flags || !done_counter) return fail(TSG_EVALUE, "tsg_mpdata_step_strip: NULL flags / counter");
-    if (step < 0 || timeout_ms < 0) return fail(TSG_EVALUE, "tsg_mpdata_step_strip: bad step / timeout");
-    if (!halo_up && !halo_down) return fail(TSG_EVALUE, "tsg_mpdata_step_strip: no neighbour halo rows");
+                                     int64_t *flag_down, int64_t step, int64_t *epoch,
+                                     int timeout_ms, int *error_word, int *done_counter,
+                                     tsg_stream s) {
     FusedLaunch L;
-    if (int rc = prepare(g, pd, vn, wn, rho, signs, dual, pd_out, dt, pivbz, flux_op, 0, g->rows,
-                         halo_up, halo_down, &L))
+    if (int rc = prepare_strip(g, pd, vn, wn, rho, signs, dual, pd_out, dt, pivbz, flux_op, halo_up,
+                               halo_down, my_flags, flag_up, flag_down, step, epoch, timeout_ms,
+                               error_word, done_counter, &L))
         return rc;
-    FusedArgs &a = L.a;
-    a.my_flags = my_flags;
-    a.flag_up = flag_up;
-    a.flag_down = flag_down;
-    a.wait_value = step;
-    a.timeout_ns = (uint64_t)timeout_ms * 1000000ull;
-    a.err = error_word;
-    a.done = done_counter;
-    a.rotate = 1;
     return launch(&L, s);
 }
 
@@ -726,7 +804,31 @@ extern "C" int tsg_mpdata_run(tsg_grid *g, double *pd_a, double *pd_b, const dou
         int n = 0;
         if (int rc = encode_pd(variants(&n)[pick_variant(g, g->rows) - 1], g, pd_b, &bwd.m_pd)) return rc;
     }
+    if (nsteps >= kGraphMinSteps) return run_pair_graph(g, fwd, bwd, nsteps, s);
     for (int t = 0; t < nsteps; ++t)
         if (int rc = launch(t % 2 == 0 ? &fwd : &bwd, s)) return rc;
     return TSG_OK;
+}
+
+extern "C" int tsg_mpdata_run_strip(tsg_grid *g, double *pd_a, double *pd_b, const double *vn,
+                                    const double *wn, const double *rho, const double *signs,
+                                    const double *dual, double dt, double pivbz, int flux_op,
+                                    double *halo_up_a, double *halo_down_a, double *halo_up_b,
+                                    double *halo_down_b, const int64_t *my_flags, int64_t *flag_up,
+                                    int64_t *flag_down, int64_t *epoch, int timeout_ms,
+                                    int *error_word, int *done_counter, int nsteps, tsg_stream s) {
+    if (!g) return fail(TSG_EVALUE, "grid is NULL");
+    if (nsteps < 0) return fail(TSG_EVALUE, "nsteps must be >= 0, got %d", nsteps);
+    if (!epoch) return fail(TSG_EVALUE, "tsg_mpdata_run_strip: the step counter must live on the device");
+    if (nsteps == 0) return TSG_OK;
+    FusedLaunch fwd, bwd;  // a -> b (halos of the neighbours' b) and b -> a
+    if (int rc = prepare_strip(g, pd_a, vn, wn, rho, signs, dual, pd_b, dt, pivbz, flux_op, halo_up_a,
+                               halo_down_a, my_flags, flag_up, flag_down, 0, epoch, timeout_ms,
+                               error_word, done_counter, &fwd))
+        return rc;
+    if (int rc = prepare_strip(g, pd_b, vn, wn, rho, signs, dual, pd_a, dt, pivbz, flux_op, halo_up_b,
+                               halo_down_b, my_flags, flag_up, flag_down, 0, epoch, timeout_ms,
+                               error_word, done_counter, &bwd))
+        return rc;
+    return run_pair_graph(g, fwd, bwd, nsteps, s);
 }

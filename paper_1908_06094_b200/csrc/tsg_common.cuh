@@ -15,7 +15,12 @@ struct tsg_grid {
     int rows, cols, levels, flags;
     int row0, global_rows;  // strip origin inside the global patch (multi-GPU); 0 / rows otherwise
     int device, num_sms;
+    void *graph;  // cached two-step CUDA graph of the time loops (mpdata_fused.cu), or NULL
 };
+
+namespace tsg {
+void destroy_graph_cache(tsg_grid *g);
+}
 
 namespace tsg {
 

@@ -182,6 +182,7 @@ class StripStepper:
         self._flags = RawBuffer((2,), dtype="<i8")
         self._err = RawBuffer((1,), dtype="<i4")
         self._done = RawBuffer((1,), dtype="<i4")  # CTA arrival counter of the strip launch
+        self._epoch = RawBuffer((1,), dtype="<i8")  # the step counter, advanced on the device
         mine = (self._raw[0].ipc_handle(), self._raw[1].ipc_handle(), self._flags.ipc_handle(),
                 self.nrows)
         every = [None] * self.world
@@ -272,8 +273,8 @@ class StripStepper:
                       _lib.ptr(self.wn), _lib.ptr(self.rho), _lib.ptr(self.signs), _lib.ptr(self.dual),
                       _lib.ptr(self.pd_out), float(dt), float(pivbz), self.flux_code, hu, hd,
                       ctypes.c_void_p(self._flags.ptr), ctypes.c_void_p(up["flags"].ptr + 8),
-                      ctypes.c_void_p(down["flags"].ptr), n, self.timeout_ms,
-                      ctypes.c_void_p(self._err.ptr), ctypes.c_void_p(self._done.ptr), s)
+                      ctypes.c_void_p(down["flags"].ptr), n, ctypes.c_void_p(self._epoch.ptr),
+                      self.timeout_ms, ctypes.c_void_p(self._err.ptr), ctypes.c_void_p(self._done.ptr), s)
             return
         self._launch(1, self.nrows - 1, dt, pivbz, main)  # interior: no halo, no peers
         # neighbours finished step n-1: my halo rows are complete and their pd_out is free
@@ -289,6 +290,40 @@ class StripStepper:
         # I am my up neighbour's down neighbour (its flag word 1) and vice versa
         _lib.call("tsg_signal_peers", ctypes.c_void_p(up["flags"].ptr + 8),
                   ctypes.c_void_p(down["flags"].ptr), n + 1, s)
+
+    def run(self, steps: int, dt: float, pivbz: float) -> None:
+        """``steps`` x (step; swap).  With the one-launch p2p exchange the loop is a captured
+        two-step CUDA graph (tsg_mpdata_run_strip): halo stores, fences and the step counter
+        all on the device, one graph launch per two steps."""
+        import ctypes
+
+        steps = int(steps)
+        if steps < 0:
+            raise ValueError(f"steps must be >= 0, got {steps}")
+        if self.mode != "p2p" or not self.single_launch or steps == 0:
+            for _ in range(steps):
+                self.step(dt, pivbz)
+                self.swap()
+            return
+        a, b = self._parity, 1 - self._parity
+        up, down = self._peers[self.strips.up(self.rank)], self._peers[self.strips.down(self.rank)]
+
+        def halos(buf):  # the neighbours' halo rows inside their buffer `buf`
+            return (ctypes.c_void_p(up["bufs"][buf].ptr + (up["nrows"] + 1) * self._rowstride),
+                    ctypes.c_void_p(down["bufs"][buf].ptr))
+
+        (hua, hda), (hub, hdb) = halos(b), halos(a)
+        _lib.call("tsg_mpdata_run_strip", self.grid.handle, ctypes.c_void_p(self._raw[a].ptr),
+                  ctypes.c_void_p(self._raw[b].ptr), _lib.ptr(self.vn), _lib.ptr(self.wn),
+                  _lib.ptr(self.rho), _lib.ptr(self.signs), _lib.ptr(self.dual), float(dt), float(pivbz),
+                  self.flux_code, hua, hda, hub, hdb, ctypes.c_void_p(self._flags.ptr),
+                  ctypes.c_void_p(up["flags"].ptr + 8), ctypes.c_void_p(down["flags"].ptr),
+                  ctypes.c_void_p(self._epoch.ptr), self.timeout_ms, ctypes.c_void_p(self._err.ptr),
+                  ctypes.c_void_p(self._done.ptr), steps, _lib.stream_handle())
+        self.steps_done += steps
+        if steps % 2:
+            self.pd, self.pd_out = self.pd_out, self.pd
+            self._parity = 1 - self._parity
 
     def check(self) -> None:
         """Raise if a step fence timed out (a neighbour never arrived)."""

@@ -131,7 +131,7 @@ def test_strip_steppers_on_one_gpu_match_single_patch(cuda_ok):
     assert torch.equal(got, single.interior("pd"))
 
 
-def _p2p_worker(rank, world, port, q, single_launch=True):
+def _p2p_worker(rank, world, port, q, single_launch=True, graph=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -141,9 +141,13 @@ def _p2p_worker(rank, world, port, q, single_launch=True):
         rows, cols, K = 17, 29, 18
         st = StripStepper(rows, cols, K, rank, world, seed=7, mode="p2p", timeout_ms=60000,
                           single_launch=single_launch)
-        for _ in range(4):
-            st.step(0.2, 0.8)
-            st.swap()
+        if graph:  # 1 + 5 steps: the captured two-step graph, an odd tail, a rebuilt graph
+            st.run(1, 0.2, 0.8)
+            st.run(5, 0.2, 0.8)
+        else:
+            for _ in range(6):
+                st.step(0.2, 0.8)
+                st.swap()
         torch.cuda.synchronize()
         st.check()
         dist.barrier()  # every rank's last step has landed in its neighbours' halos
@@ -153,7 +157,7 @@ def _p2p_worker(rank, world, port, q, single_launch=True):
         ok = None
         if rank == 0:
             single = StripStepper(rows, cols, K, 0, 1, seed=7)
-            for _ in range(4):
+            for _ in range(6):
                 single.step(0.2, 0.8)
                 single.swap()
             want = single.interior("pd").cpu()
@@ -165,8 +169,9 @@ def _p2p_worker(rank, world, port, q, single_launch=True):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,single_launch", [(2, True), (2, False), (3, True)])
-def test_p2p_fused_exchange_processes_share_one_gpu(cuda_ok, world, single_launch):
+@pytest.mark.parametrize("world,single_launch,graph", [(2, True, False), (2, False, False),
+                                                       (3, True, False), (2, True, True)])
+def test_p2p_fused_exchange_processes_share_one_gpu(cuda_ok, world, single_launch, graph):
     """Ranks (processes) on one GPU: IPC-mapped density buffers, boundary rows stored
     straight into the neighbour's halo by the step kernel, device-side step fence -- the
     multi-GPU fused-exchange path end to end, as one launch per step (in-kernel fence and
@@ -174,7 +179,7 @@ def test_p2p_fused_exchange_processes_share_one_gpu(cuda_ok, world, single_launc
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, q, single_launch))
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, q, single_launch, graph))
              for r in range(world)]
     for p in procs:
         p.start()
