@@ -261,7 +261,8 @@ def test_device_halo_update_matches_host(cuda_ok):
 
 
 @pytest.mark.parametrize("shape", [(6, 5, 2), (6, 5, 137), (2, 2, 3), (11, 3, 17), (4, 70, 81),
-                                   (5, 9, 63), (7, 6, 64), (3, 17, 65)])  # the pitch-16 threshold
+                                   (5, 9, 63), (7, 6, 64), (3, 17, 65),  # the pitch-16 threshold
+                                   (5, 4, 301)])  # a long column: 19 chunks, odd
 def test_edge_shapes_fused_unfused_indirect(cuda_ok, shape):
     from tests.gpu_helpers import fused_step, oracle_tables, unfused_step
 
