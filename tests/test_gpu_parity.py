@@ -114,8 +114,9 @@ def test_multistep_time_loop_matches_reference_hash(cuda_ok, golden_hashes):
         st.swap()
     st.swap()
     assert sha(st.download()) == e["outputs"]["pd_out"]
-    # the same loop as one device ping-pong (tsg_mpdata_run), odd and even counts
-    for split in ((e["steps"],), (3, e["steps"] - 3)):
+    # the same loop as one device ping-pong (tsg_mpdata_run), odd and even counts; from 4
+    # steps a captured two-step graph, reused in either orientation across calls
+    for split in ((e["steps"],), (3, e["steps"] - 3), (5, 4, 1), (4, 4, 2), (1, 5, 4)):
         st = stepper_for(44, 72, 10, inp)
         for n in split:
             st.run(n, e["dt"], e["pivbz"])
