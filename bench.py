@@ -206,6 +206,8 @@ def run_ours(args):
         dist.init_process_group("gloo" if shared else "nccl")
     if args.variant:
         _lib.call("tsg_set_fused_variant", args.variant)
+    if args.no_band:
+        _lib.call("tsg_set_fused_band", 0)
 
     def barrier():
         if world > 1:
@@ -337,6 +339,7 @@ def run_ours(args):
 
     vi = [ctypes.c_int() for _ in range(6)]
     variant = _l().tsg_fused_variant_of(stepper.grid.handle, 0, my_rows)
+    band = world == 1 and _l().tsg_fused_band_of(stepper.grid.handle, 0, my_rows) == 1
     _l().tsg_fused_variant_info(variant, *[ctypes.byref(x) for x in vi])
     cpu = None
     if not args.no_cpu and world == 1:  # the host baseline is measured at N = 1 only
@@ -362,6 +365,7 @@ def run_ours(args):
                                      "neighbours' halos (CUDA IPC over NVLink), in-kernel step fence"
                                      if args.exchange == "p2p" else "NCCL grouped send/recv"),
                    "l2": "256 MiB read-only L2 flush before every timed step (outside the events)",
+                   "fused_schedule": ("band round robin" if band else "contiguous ranges"),
                    "fused_tile": {"variant": variant, "ti": vi[0].value, "tj": vi[1].value, "kc": vi[2].value,
                                   "stages": vi[3].value, "threads": vi[4].value,
                                   "smem_bytes": vi[5].value}},
@@ -393,6 +397,8 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--variant", type=int, default=0, help="fused tile variant (0 = default)")
+    ap.add_argument("--no-band", action="store_true",
+                    help="disable the band schedule of large patches (tall tiles instead)")
     ap.add_argument("--exchange", choices=("p2p", "nccl"), default="p2p",
                     help="N>1 halo exchange: fused P2P epilogue stores (default) or NCCL send/recv")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3",

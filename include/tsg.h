@@ -187,6 +187,12 @@ int tsg_fused_variant_info(int variant, int *ti, int *tj, int *kc, int *stages, 
                            int *smem_bytes);
 /* The variant a fused launch over logical rows [row_lo, row_hi) of `g` uses (-1 on error). */
 int tsg_fused_variant_of(const tsg_grid *g, int row_lo, int row_hi);
+/* Whether that launch (single-GPU, no peer rows) deals whole tiles round robin in
+ * band-major order (1) or walks contiguous ranges (0): the band schedule replaces the tall
+ * tile when the tile above would be evicted from L2 and every CTA gets >= 16 tiles. */
+int tsg_fused_band_of(const tsg_grid *g, int row_lo, int row_hi);
+/* Enable (1, default) or disable (0) that band schedule. */
+int tsg_set_fused_band(int on);
 
 /* ---- neighbour reductions (stencil.py:401-408; kernels.py:27-104; reference.py:137-157) */
 /* Structured ("direct") reduce for any of the 9 relations (connectivity.py:36-68):

@@ -32,6 +32,11 @@
 //  * No tensor cores: fp64 stencil, ~0.5 flop/byte, the HBM roofline bounds it.
 #include <string.h>
 
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+
 #include "tsg_tma.cuh"
 
 namespace tsg {
@@ -93,6 +98,32 @@ struct FusedArgs {
     int64_t units;
 };
 
+// BAND schedule (large patches, single-GPU launches): whole tiles dealt round robin in
+// band-major order (bands of band_w tile columns, tile rows within a band), each CTA
+// running all chunks of its tile back to back (the per-tile state stays in registers).
+// The tiles in flight at any time are ~G consecutive tiles of that order, so the tile
+// above a tile (band_w tiles earlier) is loaded at the same time by another CTA and the
+// halo rows they share are read from DRAM once.  A separate kernel parameter: the
+// contiguous instantiations compile exactly as without it.
+struct BandArgs {
+    int band_w, nb_full;
+    uint32_t full_tiles;
+    FastDiv fd_band_tiles, fd_bw, fd_bw_last;
+};
+
+__device__ __forceinline__ void band_tile(uint32_t t, const BandArgs &b, int &ti, int &tj) {
+    if (t < b.full_tiles) {
+        const uint32_t band = b.fd_band_tiles.div(t), r = t - band * b.fd_band_tiles.d;
+        const uint32_t row = b.fd_bw.div(r);
+        ti = (int)row;
+        tj = (int)(band * b.band_w + (r - row * b.fd_bw.d));
+    } else {
+        const uint32_t r = t - b.full_tiles, row = b.fd_bw_last.div(r);
+        ti = (int)row;
+        tj = b.nb_full * b.band_w + (int)(r - row * b.fd_bw_last.d);
+    }
+}
+
 __device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
     int64_t v;
     asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -125,12 +156,13 @@ __device__ inline void wait_both(const int64_t *flags, int64_t value, uint64_t t
 // the shared interface flux k+1 computed once, half the per-unit overhead per point.
 // PEER: the launch stores its strip's boundary rows into the ring neighbours' halo rows
 // (a separate instantiation so the single-GPU kernel carries none of that epilogue)
-template <int TI, int TJ, int KC, int STAGES, int LV, int LP, int OP, bool PEER = false>
+template <int TI, int TJ, int KC, int STAGES, int LV, int LP, int OP, bool PEER = false, bool BAND = false>
 __global__ void __launch_bounds__(TI *TJ * LV, 1)
     mpdata_fused_kernel(const __grid_constant__ CUtensorMap tm_pd,
                         const __grid_constant__ CUtensorMap tm_vn,
                         const __grid_constant__ CUtensorMap tm_wn,
-                        const __grid_constant__ CUtensorMap tm_rho, const FusedArgs a) {
+                        const __grid_constant__ CUtensorMap tm_rho, const FusedArgs a,
+                        const BandArgs ba) {
     using C = FusedCfg<TI, TJ, KC, STAGES, LV, LP>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * C::kStageBytes);
@@ -152,9 +184,10 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
     const int oR = (li * TJ + lj) * KC + kq;
 
     // contiguous unit range of this CTA; unit = tile * chunks + chunk (tile-major)
-    const int u_begin = (int)(a.units * blockIdx.x / gridDim.x);
-    const int u_end = (int)(a.units * (blockIdx.x + 1) / gridDim.x);
-    const int n_units = u_end - u_begin;
+    // (BAND: tiles blockIdx.x, blockIdx.x + G, ... of the band order, all their chunks)
+    const int u_begin = BAND ? 0 : (int)(a.units * blockIdx.x / gridDim.x);
+    const int n_units = BAND ? (int)((a.tiles_i * a.tiles_j - blockIdx.x + gridDim.x - 1) / gridDim.x) * a.chunks
+                             : (int)(a.units * (blockIdx.x + 1) / gridDim.x) - u_begin;
 
     if (tid == 0) {
         prefetch_tmap(&tm_pd);
@@ -182,6 +215,8 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
     // producer cursor (thread 0 only), decoded once, then advanced incrementally
     int p_chunk = u_begin % a.chunks, p_tile = u_begin / a.chunks;
     int p_ti = p_tile / a.tiles_j, p_tj = p_tile % a.tiles_j;
+    uint32_t p_band_t = blockIdx.x;  // BAND: the producer's tile in the band order
+    if constexpr (BAND) band_tile(p_band_t, ba, p_ti, p_tj);
     auto issue_next = [&](int stage) {
         const int tr = tile_row(p_ti);
         if constexpr (PEER) {
@@ -201,7 +236,10 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
         tma_load_3d(base + C::kRhoOff, &tm_rho, bar, k0, j0 + 1, i0 + 1);
         if (++p_chunk == a.chunks) {
             p_chunk = 0;
-            if (++p_tj == a.tiles_j) {
+            if constexpr (BAND) {
+                p_band_t += gridDim.x;
+                band_tile(p_band_t, ba, p_ti, p_tj);
+            } else if (++p_tj == a.tiles_j) {
                 p_tj = 0;
                 ++p_ti;
             }
@@ -215,6 +253,8 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
     // consumer cursor
     int chunk = u_begin % a.chunks, tile = u_begin / a.chunks;
     int ti = tile / a.tiles_j, tj = tile % a.tiles_j;
+    uint32_t band_t = blockIdx.x;
+    if constexpr (BAND) band_tile(band_t, ba, ti, tj);
     const int64_t pv = pitch_of(a.K), rowstride = (int64_t)(a.cols + 2) * pv;
     const int last_chunk = a.chunks - 1;
 
@@ -398,7 +438,10 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
     next_unit:
         if (++chunk == a.chunks) {
             chunk = 0;
-            if (++tj == a.tiles_j) {
+            if constexpr (BAND) {
+                band_t += gridDim.x;
+                band_tile(band_t, ba, ti, tj);
+            } else if (++tj == a.tiles_j) {
                 tj = 0;
                 ++ti;
             }
@@ -427,6 +470,7 @@ struct Variant {
     int threads, smem;
     void *fn[4];    // upwind, centred, data-movement probe, compute probe
     void *peer[2];  // upwind, centred with the fused halo-row stores
+    void *band[2];  // upwind, centred under the BAND schedule
 };
 
 template <int TI, int TJ, int KC, int STAGES, int LV = 16, int LP = 1>
@@ -445,6 +489,11 @@ static Variant make_variant() {
     v.fn[3] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, kComputeProbe>;
     v.peer[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND, true>;
     v.peer[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED, true>;
+    v.band[0] = v.band[1] = nullptr;
+    if constexpr (LP == 2) {  // the level-pair variants only (the default and its kin)
+        v.band[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND, false, true>;
+        v.band[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED, false, true>;
+    }
     return v;
 }
 
@@ -488,8 +537,27 @@ constexpr int kGraphMinSteps = 4;  // tsg_mpdata_run replays a captured two-step
 constexpr double kReuseUnits = 8.0;
 static int g_variant = 0;  // 0 = choose per launch (pick_variant)
 
+// The BAND schedule for patches whose tile above is evicted under the contiguous schedule
+// (O1280, 2560x2576x137: 9.56-9.65 ms vs 10.13 ms with the tall tile, same box; DRAM
+// reads 48.2 GB vs 56.3 GB, ncu).  tsg_set_fused_band(0) falls back to the tall tile.
+static int g_band = 1;
+static bool band_enabled() { return g_band != 0; }
+
+static bool evicted(const tsg_grid *g, int nrows) {
+    int n = 0;
+    const Variant &v = variants(&n)[kCompactVariant - 1];
+    const double tiles_j = (g->cols + v.tj - 1) / v.tj, chunks = (g->levels + v.kc - 1) / v.kc;
+    const double units = (double)((nrows + v.ti - 1) / v.ti) * tiles_j * chunks;
+    const double range = units / g->num_sms, R = tiles_j * chunks;
+    const double gap = R < range ? R : R - range * (double)(int64_t)(R / range);
+    return gap > kReuseUnits;
+}
+
+constexpr int kBandTiles = 16;  // BAND schedule: tile columns per band
+
 static int pick_variant(const tsg_grid *g, int nrows) {
     if (g_variant) return g_variant;
+    if (band_enabled() && evicted(g, nrows)) return kCompactVariant;  // with the BAND schedule
     int n = 0;
     const Variant &v = variants(&n)[kCompactVariant - 1];
     const double tiles_j = (g->cols + v.tj - 1) / v.tj, chunks = (g->levels + v.kc - 1) / v.kc;
@@ -527,6 +595,28 @@ extern "C" int tsg_fused_variant_info(int variant, int *ti, int *tj, int *kc, in
     return TSG_OK;
 }
 
+extern "C" int tsg_set_fused_band(int on) {
+    if (on != 0 && on != 1) return fail(TSG_EVALUE, "fused band schedule switch must be 0 or 1, got %d", on);
+    g_band = on;
+    return TSG_OK;
+}
+
+extern "C" int tsg_fused_band_of(const tsg_grid *g, int row_lo, int row_hi) {
+    if (!g) {
+        fail(TSG_EVALUE, "grid is NULL");
+        return -1;
+    }
+    if (row_lo < 0 || row_hi > g->rows || row_lo > row_hi) {
+        fail(TSG_EVALUE, "row range [%d, %d) outside [0, %d)", row_lo, row_hi, g->rows);
+        return -1;
+    }
+    int n = 0;
+    const Variant &v = variants(&n)[pick_variant(g, row_hi - row_lo) - 1];
+    const int64_t tiles = (int64_t)((row_hi - row_lo + v.ti - 1) / v.ti) * ((g->cols + v.tj - 1) / v.tj);
+    return (!g_variant && v.band[0] && band_enabled() && evicted(g, row_hi - row_lo) &&
+            tiles >= 16LL * g->num_sms) ? 1 : 0;
+}
+
 extern "C" int tsg_fused_variant_of(const tsg_grid *g, int row_lo, int row_hi) {
     if (!g) {
         fail(TSG_EVALUE, "grid is NULL");
@@ -560,6 +650,7 @@ extern "C" int tsg_mpdata_step_rows(tsg_grid *g, const double *pd, const double 
 struct FusedLaunch {
     CUtensorMap m_pd, m_vn, m_wn, m_rho;
     FusedArgs a;
+    BandArgs ba;
     void *fn;
     int grid, threads, smem;
 };
@@ -658,6 +749,24 @@ static int prepare(tsg_grid *g, const double *pd, const double *vn, const double
         return fail(TSG_EVALUE, "the probes do not exchange halo rows");
     L->fn = peer ? v.peer[flux_op]
                  : v.fn[flux_op == kProbeOp ? 2 : (flux_op == kComputeProbe ? 3 : flux_op)];
+    // the BAND schedule: single-GPU launches of a patch whose tile above is evicted under the
+    // contiguous schedule, when every CTA gets many tiles (the deal is whole tiles)
+    const bool band = !g_variant && !peer && flux_op <= TSG_CENTRED && v.band[0] && band_enabled() &&
+                      evicted(g, row_hi - row_lo) &&
+                      (int64_t)tiles_i * a.tiles_j >= 16LL * g->num_sms;
+    if (band) {
+        L->fn = v.band[flux_op];
+        BandArgs &b = L->ba;
+        b.band_w = std::min(kBandTiles, a.tiles_j);
+        b.nb_full = a.tiles_j / b.band_w;
+        const int bw_last = a.tiles_j - b.nb_full * b.band_w;
+        b.full_tiles = (uint32_t)(b.nb_full * b.band_w * tiles_i);
+        b.fd_band_tiles = FastDiv((uint32_t)(b.band_w * tiles_i));
+        b.fd_bw = FastDiv((uint32_t)b.band_w);
+        b.fd_bw_last = FastDiv((uint32_t)(bw_last > 0 ? bw_last : 1));
+    } else {
+        memset(&L->ba, 0, sizeof(L->ba));
+    }
     TSG_CHECK_CUDA(cudaFuncSetAttribute(L->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
     int per_sm = 0;
     TSG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L->fn, v.threads, v.smem));
@@ -672,7 +781,7 @@ static int prepare(tsg_grid *g, const double *pd, const double *vn, const double
 
 static int launch(FusedLaunch *L, tsg_stream s) {
     if (L->a.units == 0) return TSG_OK;
-    void *args[] = {&L->m_pd, &L->m_vn, &L->m_wn, &L->m_rho, &L->a};
+    void *args[] = {&L->m_pd, &L->m_vn, &L->m_wn, &L->m_rho, &L->a, &L->ba};
     TSG_CHECK_CUDA(cudaLaunchKernel(L->fn, dim3((unsigned)L->grid), dim3(L->threads), args, L->smem,
                                     (cudaStream_t)s));
     return TSG_OK;

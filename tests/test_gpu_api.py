@@ -324,15 +324,24 @@ def test_extreme_dual_volumes(cuda_ok):
 
 
 def test_default_fused_variant_follows_the_l2_reuse_rule(cuda_ok):
-    """Variant 0 picks the compact 4x16 tile when the tile above is still in L2 under the
-    contiguous schedule (the bench patch) and the tall 16x4 tile otherwise (O1280-class)."""
+    """Variant 0 keeps the compact 4x16 tile on contiguous ranges when the tile above is still
+    in L2 (the bench patch); otherwise (O1280-class) the band schedule, or with it disabled
+    the tall 16x4 tile."""
     from paper_1908_06094_b200 import _lib
     from paper_1908_06094_b200.device import DeviceGrid
 
     lib = _lib.lib()
     bench, big = DeviceGrid(279, 256, 80), DeviceGrid(2560, 2576, 137)
     assert lib.tsg_fused_variant_of(bench.handle, 0, 279) == 15
-    assert lib.tsg_fused_variant_of(big.handle, 0, 2560) == 19
+    assert lib.tsg_fused_band_of(bench.handle, 0, 279) == 0
+    assert lib.tsg_fused_variant_of(big.handle, 0, 2560) == 15
+    assert lib.tsg_fused_band_of(big.handle, 0, 2560) == 1
+    _lib.call("tsg_set_fused_band", 0)
+    try:
+        assert lib.tsg_fused_variant_of(big.handle, 0, 2560) == 19
+        assert lib.tsg_fused_band_of(big.handle, 0, 2560) == 0
+    finally:
+        _lib.call("tsg_set_fused_band", 1)
     _lib.call("tsg_set_fused_variant", 18)
     try:
         assert lib.tsg_fused_variant_of(bench.handle, 0, 279) == 18
