@@ -105,21 +105,30 @@ struct FusedArgs {
 // above a tile (band_w tiles earlier) is loaded at the same time by another CTA and the
 // halo rows they share are read from DRAM once.  A separate kernel parameter: the
 // contiguous instantiations compile exactly as without it.
+// A row strip (PEER launches) bands its interior tile rows 1 .. T-2 only and deals the two
+// boundary tile rows last (row T-1, then row 0), so only the final tiles wait for the
+// neighbours' step flags.
 struct BandArgs {
     int band_w, nb_full;
     uint32_t full_tiles;
     FastDiv fd_band_tiles, fd_bw, fd_bw_last;
+    int row_base, tiles_i, tiles_j;  // first banded tile row; the launch's tile grid
+    uint32_t banded;                 // tiles in the band order (the rest: boundary rows)
 };
 
 __device__ __forceinline__ void band_tile(uint32_t t, const BandArgs &b, int &ti, int &tj) {
-    if (t < b.full_tiles) {
+    if (t >= b.banded) {  // the boundary tile rows of a strip
+        const int r = (int)(t - b.banded);
+        ti = r < b.tiles_j ? b.tiles_i - 1 : 0;
+        tj = r < b.tiles_j ? r : r - b.tiles_j;
+    } else if (t < b.full_tiles) {
         const uint32_t band = b.fd_band_tiles.div(t), r = t - band * b.fd_band_tiles.d;
         const uint32_t row = b.fd_bw.div(r);
-        ti = (int)row;
+        ti = b.row_base + (int)row;
         tj = (int)(band * b.band_w + (r - row * b.fd_bw.d));
     } else {
         const uint32_t r = t - b.full_tiles, row = b.fd_bw_last.div(r);
-        ti = (int)row;
+        ti = b.row_base + (int)row;
         tj = b.nb_full * b.band_w + (int)(r - row * b.fd_bw_last.d);
     }
 }
@@ -205,7 +214,7 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
 
     // sequence tile row -> tile row: with `rotate` the boundary tile rows come last
     // (order 1, 2, ..., T-1, 0) so only the final units wait for the neighbours
-    auto tile_row = [&](int t) { return (PEER && a.rotate) ? (t + 1 == a.tiles_i ? 0 : t + 1) : t; };
+    auto tile_row = [&](int t) { return (PEER && !BAND && a.rotate) ? (t + 1 == a.tiles_i ? 0 : t + 1) : t; };
     bool waited = !(PEER && a.my_flags);
     int64_t wv = a.wait_value;  // the step this launch performs
     if constexpr (PEER) {
@@ -470,7 +479,8 @@ struct Variant {
     int threads, smem;
     void *fn[4];    // upwind, centred, data-movement probe, compute probe
     void *peer[2];  // upwind, centred with the fused halo-row stores
-    void *band[2];  // upwind, centred under the BAND schedule
+    void *band[2];      // upwind, centred under the BAND schedule
+    void *peer_band[2];  // the same with the fused halo-row stores (row strips)
 };
 
 template <int TI, int TJ, int KC, int STAGES, int LV = 16, int LP = 1>
@@ -489,10 +499,12 @@ static Variant make_variant() {
     v.fn[3] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, kComputeProbe>;
     v.peer[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND, true>;
     v.peer[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED, true>;
-    v.band[0] = v.band[1] = nullptr;
+    v.band[0] = v.band[1] = v.peer_band[0] = v.peer_band[1] = nullptr;
     if constexpr (LP == 2) {  // the level-pair variants only (the default and its kin)
         v.band[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND, false, true>;
         v.band[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED, false, true>;
+        v.peer_band[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND, true, true>;
+        v.peer_band[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED, true, true>;
     }
     return v;
 }
@@ -554,6 +566,23 @@ static bool evicted(const tsg_grid *g, int nrows) {
 }
 
 constexpr int kBandTiles = 16;  // BAND schedule: tile columns per band
+
+// band-major order of a launch's tiles; a strip bands rows 1 .. T-2 and deals its two
+// boundary tile rows last
+static void fill_band(BandArgs &b, int tiles_i, int tiles_j, bool strip) {
+    const int rows = strip ? tiles_i - 2 : tiles_i;
+    b.row_base = strip ? 1 : 0;
+    b.tiles_i = tiles_i;
+    b.tiles_j = tiles_j;
+    b.banded = (uint32_t)rows * (uint32_t)tiles_j;
+    b.band_w = std::min(kBandTiles, tiles_j);
+    b.nb_full = tiles_j / b.band_w;
+    const int bw_last = tiles_j - b.nb_full * b.band_w;
+    b.full_tiles = (uint32_t)(b.nb_full * b.band_w * rows);
+    b.fd_band_tiles = FastDiv((uint32_t)(b.band_w * rows));
+    b.fd_bw = FastDiv((uint32_t)b.band_w);
+    b.fd_bw_last = FastDiv((uint32_t)(bw_last > 0 ? bw_last : 1));
+}
 
 static int pick_variant(const tsg_grid *g, int nrows) {
     if (g_variant) return g_variant;
@@ -754,18 +783,10 @@ static int prepare(tsg_grid *g, const double *pd, const double *vn, const double
     const bool band = !g_variant && !peer && flux_op <= TSG_CENTRED && v.band[0] && band_enabled() &&
                       evicted(g, row_hi - row_lo) &&
                       (int64_t)tiles_i * a.tiles_j >= 16LL * g->num_sms;
+    memset(&L->ba, 0, sizeof(L->ba));
     if (band) {
         L->fn = v.band[flux_op];
-        BandArgs &b = L->ba;
-        b.band_w = std::min(kBandTiles, a.tiles_j);
-        b.nb_full = a.tiles_j / b.band_w;
-        const int bw_last = a.tiles_j - b.nb_full * b.band_w;
-        b.full_tiles = (uint32_t)(b.nb_full * b.band_w * tiles_i);
-        b.fd_band_tiles = FastDiv((uint32_t)(b.band_w * tiles_i));
-        b.fd_bw = FastDiv((uint32_t)b.band_w);
-        b.fd_bw_last = FastDiv((uint32_t)(bw_last > 0 ? bw_last : 1));
-    } else {
-        memset(&L->ba, 0, sizeof(L->ba));
+        fill_band(L->ba, tiles_i, a.tiles_j, false);
     }
     TSG_CHECK_CUDA(cudaFuncSetAttribute(L->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
     int per_sm = 0;
@@ -823,6 +844,16 @@ static int prepare_strip(tsg_grid *g, const double *pd, const double *vn, const 
     a.err = error_word;
     a.done = done_counter;
     a.rotate = 1;
+    // the band schedule for a large strip (its tile above evicted under contiguous ranges)
+    int n = 0;
+    const int vi = pick_variant(g, g->rows);
+    const Variant &v = variants(&n)[vi - 1];
+    if (!g_variant && v.peer_band[0] && band_enabled() && evicted(g, g->rows) && a.tiles_i >= 3 &&
+        (int64_t)a.tiles_i * a.tiles_j >= 16LL * g->num_sms && flux_op <= TSG_CENTRED) {
+        L->fn = v.peer_band[flux_op];
+        TSG_CHECK_CUDA(cudaFuncSetAttribute(L->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
+        fill_band(L->ba, a.tiles_i, a.tiles_j, true);
+    }
     return TSG_OK;
 }
 

@@ -131,14 +131,14 @@ def test_strip_steppers_on_one_gpu_match_single_patch(cuda_ok):
     assert torch.equal(got, single.interior("pd"))
 
 
-def _p2p_worker(rank, world, port, q, single_launch=True, graph=False):
+def _p2p_worker(rank, world, port, q, single_launch=True, graph=False, shape=(17, 29, 18)):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1908_06094_b200.distributed import StripStepper
 
-        rows, cols, K = 17, 29, 18
+        rows, cols, K = shape
         st = StripStepper(rows, cols, K, rank, world, seed=7, mode="p2p", timeout_ms=60000,
                           single_launch=single_launch)
         if graph:  # 1 + 5 steps: the captured two-step graph, an odd tail, a rebuilt graph
@@ -169,9 +169,12 @@ def _p2p_worker(rank, world, port, q, single_launch=True, graph=False):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,single_launch,graph", [(2, True, False), (2, False, False),
-                                                       (3, True, False), (2, True, True)])
-def test_p2p_fused_exchange_processes_share_one_gpu(cuda_ok, world, single_launch, graph):
+@pytest.mark.parametrize("world,single_launch,graph,shape", [
+    (2, True, False, (17, 29, 18)), (2, False, False, (17, 29, 18)), (3, True, False, (17, 29, 18)),
+    (2, True, True, (17, 29, 18)),
+    # strips large enough for the band schedule (interior rows banded, boundary rows last)
+    (2, True, True, (512, 608, 32))])
+def test_p2p_fused_exchange_processes_share_one_gpu(cuda_ok, world, single_launch, graph, shape):
     """Ranks (processes) on one GPU: IPC-mapped density buffers, boundary rows stored
     straight into the neighbour's halo by the step kernel, device-side step fence -- the
     multi-GPU fused-exchange path end to end, as one launch per step (in-kernel fence and
@@ -179,7 +182,7 @@ def test_p2p_fused_exchange_processes_share_one_gpu(cuda_ok, world, single_launc
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, q, single_launch, graph))
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, q, single_launch, graph, shape))
              for r in range(world)]
     for p in procs:
         p.start()
