@@ -146,6 +146,9 @@ int tsg_mpdata_step_strip(tsg_grid *g, const double *pd, const double *vn, const
  * such steps ping-ponging pd_a / pd_b (halo_*_a: the neighbours' halo rows in their b
  * buffer, written while stepping a -> b; halo_*_b likewise for b -> a) as a captured
  * two-step CUDA graph (cached on the grid handle), halo exchange and fences included. */
+/* Number of time-loop graphs instantiated so far in this process (a diagnostic: a loop
+ * that alternates between the same two buffers reuses one graph). */
+int tsg_time_loop_graphs_built(void);
 int tsg_mpdata_run_strip(tsg_grid *g, double *pd_a, double *pd_b, const double *vn,
                          const double *wn, const double *rho, const double *signs,
                          const double *dual, double dt, double pivbz, int flux_op,

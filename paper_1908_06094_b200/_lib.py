@@ -58,6 +58,7 @@ SIGNATURES = {
     "tsg_fused_variant_of": (_c_int, [_p, _c_int, _c_int]),
     "tsg_fused_band_of": (_c_int, [_p, _c_int, _c_int]),
     "tsg_set_fused_band": (_c_int, [_c_int]),
+    "tsg_time_loop_graphs_built": (_c_int, []),
     "tsg_fused_variant_info": (_c_int, [_c_int] + [ctypes.POINTER(_c_int)] * 6),
     "tsg_neighbor_reduce": (_c_int, [_p, _c_int, _c_int, _c_int, _p, _p, _p, _p]),
     "tsg_neighbor_reduce_indirect": (_c_int, [_p, _c_i64, _c_int, _c_int, _p, _p, _p, _p]),

@@ -698,6 +698,7 @@ static int prepare(tsg_grid *g, const double *pd, const double *vn, const double
                    const double *rho, const double *signs, const double *dual, double *pd_out,
                    double dt, double pivbz, int flux_op, int row_lo, int row_hi, double *halo_up,
                    double *halo_down, FusedLaunch *L) {
+    memset(L, 0, sizeof(*L));  // deterministic bytes: the time-loop graph cache compares them
     if (!g) return fail(TSG_EVALUE, "grid is NULL");
     if ((halo_up || halo_down) && (g->flags & TSG_PERIODIC_ROWS))
         return fail(TSG_EVALUE, "peer halo rows need a row strip (no periodic rows)");
@@ -863,8 +864,33 @@ static int prepare_strip(tsg_grid *g, const double *pd, const double *vn, const 
 // are captured once into a graph and replayed: one graph launch per two steps, no per-step
 // host work.  The executable graph is cached on the grid handle and rebuilt when the
 // arguments change.
+// what a captured pair depends on: the loop's arguments (buffers in a -> b order), the
+// library's variant / schedule switches (a tensor map's bytes are not reproducible, so the
+// launches themselves are not compared)
+struct GraphKey {
+    const void *p[17];
+    double dt, pivbz;
+    int flux_op, timeout_ms, variant, band;
+    bool operator==(const GraphKey &o) const { return !memcmp(this, &o, sizeof(*this)); }
+};
+
+static GraphKey graph_key(const void *const *ptrs, int n, double dt, double pivbz, int flux_op,
+                          int timeout_ms) {
+    GraphKey k;
+    memset(&k, 0, sizeof(k));
+    for (int q = 0; q < n; ++q) k.p[q] = ptrs[q];
+    k.dt = dt;
+    k.pivbz = pivbz;
+    k.flux_op = flux_op;
+    k.timeout_ms = timeout_ms;
+    k.variant = g_variant;
+    k.band = g_band;
+    return k;
+}
+
 struct GraphCache {
-    FusedLaunch fwd, bwd;  // the captured pair (compared bytewise to detect a change)
+    GraphKey key;          // of the captured (fwd, bwd) pair
+    FusedLaunch fwd, bwd;  // the captured launches (for an odd tail / the swapped orientation)
     cudaGraphExec_t exec;
 };
 
@@ -877,20 +903,23 @@ void tsg::destroy_graph_cache(tsg_grid *g) {
     g->graph = nullptr;
 }
 
-static int run_pair_graph(tsg_grid *g, const FusedLaunch &fwd, const FusedLaunch &bwd, int nsteps,
-                          tsg_stream s) {
+static int g_graph_builds = 0;  // instantiated time-loop graphs (tsg_time_loop_graphs_built)
+
+// `key` describes (fwd, bwd); `swapped` the same loop started from the other buffer
+static int run_pair_graph(tsg_grid *g, const GraphKey &key, const GraphKey &swapped,
+                          const FusedLaunch &fwd, const FusedLaunch &bwd, int nsteps, tsg_stream s) {
     GraphCache *c = static_cast<GraphCache *>(g->graph);
-    auto same = [](const FusedLaunch &x, const FusedLaunch &y) { return !memcmp(&x, &y, sizeof(x)); };
-    if (c && same(c->fwd, bwd) && same(c->bwd, fwd)) {
+    if (c && c->key == swapped) {
         // the cached pair in the other orientation (a time loop after an odd number of
         // steps): one direct launch, then the graph from its first step
         if (int rc = launch(&c->bwd, s)) return rc;
         --nsteps;
-    } else if (!c || !same(c->fwd, fwd) || !same(c->bwd, bwd)) {
+    } else if (!c || !(c->key == key)) {
         destroy_graph_cache(g);
         cudaStream_t cap;
         TSG_CHECK_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
         c = new GraphCache;
+        c->key = key;
         c->fwd = fwd;
         c->bwd = bwd;
         cudaGraph_t graph = nullptr;
@@ -908,6 +937,7 @@ static int run_pair_graph(tsg_grid *g, const FusedLaunch &fwd, const FusedLaunch
             return fail(TSG_ECUDA, "time-loop graph capture failed: %s", cudaGetErrorString(e));
         }
         g->graph = c;
+        ++g_graph_builds;
     }
     for (int t = 0; t + 1 < nsteps; t += 2)
         TSG_CHECK_CUDA(cudaGraphLaunch(c->exec, (cudaStream_t)s));
@@ -950,7 +980,12 @@ extern "C" int tsg_mpdata_run(tsg_grid *g, double *pd_a, double *pd_b, const dou
         int n = 0;
         if (int rc = encode_pd(variants(&n)[pick_variant(g, g->rows) - 1], g, pd_b, &bwd.m_pd)) return rc;
     }
-    if (nsteps >= kGraphMinSteps) return run_pair_graph(g, fwd, bwd, nsteps, s);
+    if (nsteps >= kGraphMinSteps) {
+        const void *ab[] = {pd_a, pd_b, vn, wn, rho, signs, dual};
+        const void *ba[] = {pd_b, pd_a, vn, wn, rho, signs, dual};
+        return run_pair_graph(g, graph_key(ab, 7, dt, pivbz, flux_op, 0), graph_key(ba, 7, dt, pivbz, flux_op, 0),
+                              fwd, bwd, nsteps, s);
+    }
     for (int t = 0; t < nsteps; ++t)
         if (int rc = launch(t % 2 == 0 ? &fwd : &bwd, s)) return rc;
     return TSG_OK;
@@ -976,5 +1011,12 @@ extern "C" int tsg_mpdata_run_strip(tsg_grid *g, double *pd_a, double *pd_b, con
                                halo_down_b, my_flags, flag_up, flag_down, 0, epoch, timeout_ms,
                                error_word, done_counter, &bwd))
         return rc;
-    return run_pair_graph(g, fwd, bwd, nsteps, s);
+    const void *ab[] = {pd_a, pd_b, vn, wn, rho, signs, dual, halo_up_a, halo_down_a, halo_up_b,
+                        halo_down_b, my_flags, flag_up, flag_down, epoch, error_word, done_counter};
+    const void *ba[] = {pd_b, pd_a, vn, wn, rho, signs, dual, halo_up_b, halo_down_b, halo_up_a,
+                        halo_down_a, my_flags, flag_up, flag_down, epoch, error_word, done_counter};
+    return run_pair_graph(g, graph_key(ab, 17, dt, pivbz, flux_op, timeout_ms),
+                          graph_key(ba, 17, dt, pivbz, flux_op, timeout_ms), fwd, bwd, nsteps, s);
 }
+
+extern "C" int tsg_time_loop_graphs_built(void) { return g_graph_builds; }

@@ -123,3 +123,27 @@ def test_multistep_time_loop_matches_reference_hash(cuda_ok, golden_hashes):
             st.swap()
         st.swap()
         assert sha(st.download()) == e["outputs"]["pd_out"], split
+
+
+def test_time_loop_graph_is_captured_once(cuda_ok):
+    """Alternating run() calls on the same two buffers reuse one captured graph (either
+    orientation, odd tails included) and keep matching the step-by-step loop."""
+    from paper_1908_06094_b200 import _lib
+    from tests.gpu_helpers import stepper_for
+
+    inp = O.transport_inputs(23, 40, 20, 5, "random", "random", "random")
+    ref, st = stepper_for(23, 40, 20, inp), stepper_for(23, 40, 20, inp)
+    lib = _lib.lib()
+    st.run(8, 0.2, 0.8)  # run(n) leaves the newest density in pd_out, like step()
+    st.swap()
+    built = lib.tsg_time_loop_graphs_built()
+    for n in (8, 9, 4, 5):
+        st.run(n, 0.2, 0.8)
+        st.swap()
+    assert lib.tsg_time_loop_graphs_built() == built
+    for _ in range(8 + 8 + 9 + 4 + 5):
+        ref.step(0.2, 0.8)
+        ref.swap()
+    st.swap()
+    ref.swap()
+    assert np.array_equal(st.download(), ref.download())
