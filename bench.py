@@ -369,6 +369,7 @@ def run_ours(args):
                    "fused_tile": {"variant": variant, "ti": vi[0].value, "tj": vi[1].value, "kc": vi[2].value,
                                   "stages": vi[3].value, "threads": vi[4].value,
                                   "smem_bytes": vi[5].value}},
+        "ms_per_step_median": statistics.median(step_ms) if step_ms else None,
         "effective_gbs": achieved,
         "paper_model_gbs": paper_model_bytes(my_rows, cols, K) / mean_step / 1e9,
         "stage_updates_per_s": GV * (6 * K + 1) / mean_step,
