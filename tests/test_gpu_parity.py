@@ -96,6 +96,22 @@ def test_fused_step_bench_sizes_match_reference_hash(cuda_ok, golden_hashes, key
     assert sha(got) == want
 
 
+NORTH_STAR_RTOL = 1e-12  # BASELINE.json north_star: fp64 fields within 1e-12 relative
+
+
+def test_north_star_tolerance_at_the_bench_size(cuda_ok):
+    """The north-star acceptance idiom (max|a-b| <= 1e-12 max|b|, the reference's own
+    tolerance form, tests/test_mpdata.py:317) on the 279x256x80 bench patch with random
+    rho; the kernels are in fact bitwise equal, so the error is 0."""
+    r, c, lev = 279, 256, 80
+    inp = O.transport_inputs(r, c, lev, 4, "random", "random", "random")
+    want = O.step_inputs(r, c, inp, 0.2, 0.8)["pd_out"]
+    got = fused_step(r, c, lev, inp, 0.2, 0.8)
+    err = np.max(np.abs(got - want)) / np.max(np.abs(want))
+    assert err <= NORTH_STAR_RTOL
+    assert err == 0.0
+
+
 def test_unfused_bench_size_matches_reference_hash(cuda_ok, golden_hashes):
     e = golden_hashes["transport"]["cfg2_rand"]
     inp = O.transport_inputs(128, 128, 80, 0, "random", "random", "one")
