@@ -12,6 +12,9 @@
  *    reference's exception type with that message (ValueError / IndexError / ...).
  *  - Device pointers are caller-owned (the library never allocates per call); a
  *    `tsg_stream` is a cudaStream_t, every launch is stream-ordered and asynchronous.
+ *  - Thread safety: calls are reentrant across grid handles; one grid handle is used by
+ *    one host thread at a time (it caches the time loops' captured graph).  The tuning
+ *    switches (tsg_set_fused_variant / _band) are process-wide benchmarking hooks.
  *  - Structured ("direct") fields live in the device layout
  *        double field[rows + 2][colors][cols + 2][tsg_inner_pitch(inner)]
  *    i.e. (row, colour, column) parallelogram indexing with a one-element periodic
