@@ -642,7 +642,7 @@ extern "C" int tsg_fused_band_of(const tsg_grid *g, int row_lo, int row_hi) {
     int n = 0;
     const Variant &v = variants(&n)[pick_variant(g, row_hi - row_lo) - 1];
     const int64_t tiles = (int64_t)((row_hi - row_lo + v.ti - 1) / v.ti) * ((g->cols + v.tj - 1) / v.tj);
-    return (!g_variant && v.band[0] && band_enabled() && evicted(g, row_hi - row_lo) &&
+    return (v.band[0] && band_enabled() && evicted(g, row_hi - row_lo) &&
             tiles >= 16LL * g->num_sms) ? 1 : 0;
 }
 
@@ -781,7 +781,7 @@ static int prepare(tsg_grid *g, const double *pd, const double *vn, const double
                  : v.fn[flux_op == kProbeOp ? 2 : (flux_op == kComputeProbe ? 3 : flux_op)];
     // the BAND schedule: single-GPU launches of a patch whose tile above is evicted under the
     // contiguous schedule, when every CTA gets many tiles (the deal is whole tiles)
-    const bool band = !g_variant && !peer && flux_op <= TSG_CENTRED && v.band[0] && band_enabled() &&
+    const bool band = !peer && flux_op <= TSG_CENTRED && v.band[0] && band_enabled() &&
                       evicted(g, row_hi - row_lo) &&
                       (int64_t)tiles_i * a.tiles_j >= 16LL * g->num_sms;
     memset(&L->ba, 0, sizeof(L->ba));
@@ -849,7 +849,7 @@ static int prepare_strip(tsg_grid *g, const double *pd, const double *vn, const 
     int n = 0;
     const int vi = pick_variant(g, g->rows);
     const Variant &v = variants(&n)[vi - 1];
-    if (!g_variant && v.peer_band[0] && band_enabled() && evicted(g, g->rows) && a.tiles_i >= 3 &&
+    if (v.peer_band[0] && band_enabled() && evicted(g, g->rows) && a.tiles_i >= 3 &&
         (int64_t)a.tiles_i * a.tiles_j >= 16LL * g->num_sms && flux_op <= TSG_CENTRED) {
         L->fn = v.peer_band[flux_op];
         TSG_CHECK_CUDA(cudaFuncSetAttribute(L->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
