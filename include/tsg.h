@@ -128,7 +128,9 @@ int tsg_mpdata_step_rows_peer(tsg_grid *g, const double *pd, const double *vn, c
                               const double *rho, const double *signs, const double *dual,
                               double *pd_out, double dt, double pivbz, int flux_op, int row_lo,
                               int row_hi, double *halo_up, double *halo_down, tsg_stream s);
-/* One whole row-strip step in ONE launch, halo exchange and step fence included: the
+/* One whole row-strip step in ONE launch, halo exchange and step fence included (the
+ * multi-GPU form of the reference's step + periodic halo_update, executors.py:74-86 /
+ * mpdata.py:319-354; the reference replaces MPI by an in-process copy): the
  * tile rows touching the strip's first / last row run last; before loading them the
  * kernel acquires `my_flags[0..1] >= step` (both ring neighbours finished step-1, so its
  * halo rows are complete and their pd_out halo rows are free), their epilogue stores the
