@@ -41,6 +41,9 @@
 
 namespace tsg {
 
+// streaming (evict-first) 16-byte store: the step's output is not re-read by this launch
+__device__ __forceinline__ void stcs2(double *p, double2 v) { __stcs(reinterpret_cast<double2 *>(p), v); }
+
 // ---- tile geometry --------------------------------------------------------------------
 
 template <int TI, int TJ, int KC, int STAGES, int LV, int LP = 1>
@@ -365,11 +368,11 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
                 val.y = sub(c.y, dvd(mul(a.dt, dvd(acd, dual)), r.y));
                 double *o = out + k;
                 if (pair) {
-                    st2(o, val);
+                    stcs2(o, val);
                     if (d_row | d_col) {
-                        if (d_row) st2(o + d_row, val);
-                        if (d_col) st2(o + d_col, val);
-                        if (d_row && d_col) st2(o + d_row + d_col, val);
+                        if (d_row) stcs2(o + d_row, val);
+                        if (d_col) stcs2(o + d_col, val);
+                        if (d_row && d_col) stcs2(o + d_row + d_col, val);
                     }
                     if (PEER && peer) {
                         st2(peer + k, val);
