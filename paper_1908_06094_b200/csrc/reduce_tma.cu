@@ -192,11 +192,18 @@ __global__ void __launch_bounds__(red_ti(loc_colors(REL % 3)) * kRedTJ * kRedLan
                 if (MODE == 1) acc = make_double2(dvd(acc.x, sc[c]), dvd(acc.y, sc[c]));
                 double *o = out[c] + k;
                 if (pair) {
-                    st2(o, acc);
+                    // contiguous ranges: streaming (evict-first) stores leave L2 to the
+                    // source's halos (Table-1 direct 1024^2: 516 vs 523 us); the band
+                    // schedule keeps its halos in L2 anyway and does better without
+                    auto put = [](double *q, double2 x) {
+                        if constexpr (BAND) st2(q, x);
+                        else __stcs(reinterpret_cast<double2 *>(q), x);
+                    };
+                    put(o, acc);
                     if (dr | dc) {
-                        if (dr) st2(o + dr, acc);
-                        if (dc) st2(o + dc, acc);
-                        if (dr && dc) st2(o + dr + dc, acc);
+                        if (dr) put(o + dr, acc);
+                        if (dc) put(o + dc, acc);
+                        if (dr && dc) put(o + dr + dc, acc);
                     }
                 } else {  // odd level count: the last level alone
                     o[0] = acc.x;
