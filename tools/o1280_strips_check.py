@@ -3,7 +3,7 @@ two row strips in two processes sharing one GPU (fused P2P exchange, one launch 
 graph-captured loop) against the single-patch step, compared bitwise through a device-side
 hash of every interior row.  Needs ~110 GB of device memory; not part of the test suite.
 
-    python tools/o1280_strips_check.py [steps]
+    python tools/o1280_strips_check.py [steps] [strips]
 """
 import os
 import socket
@@ -52,16 +52,18 @@ def worker(rank, world, port, steps, q):
 
 if __name__ == "__main__":
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+    world = int(sys.argv[2]) if len(sys.argv) > 2 else 2
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=worker, args=(r, 2, port, steps, q)) for r in range(2)]
+    ps = [ctx.Process(target=worker, args=(r, world, port, steps, q)) for r in range(world)]
     for p in ps:
         p.start()
     ok = q.get(timeout=3000)
     for p in ps:
         p.join()
-    print(f"O1280 {ROWS}x{COLS}x{K}, 2 strips vs single patch, {steps} steps: bitwise {'EQUAL' if ok else 'DIFFERENT'}")
+    print(f"O1280 {ROWS}x{COLS}x{K}, {world} strips vs single patch, {steps} steps: "
+          f"bitwise {'EQUAL' if ok else 'DIFFERENT'}")
