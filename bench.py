@@ -218,6 +218,19 @@ def run_ours(args):
     global_rows = w["rows"] * world if w["scaling"] == "weak" else w["rows"]
     GV = global_rows * cols  # vertices of the whole job
     host_fed = args.workload == "cfg3" and world == 1
+    exchange_note = None
+    if world > 1 and not shared and args.exchange == "p2p":
+        # the fused exchange stores into the neighbours' memory: it needs peer access
+        # (NVLink / NVSwitch); without it the NCCL send/recv exchange runs instead
+        nbrs = {(local + 1) % world, (local - 1) % world} - {local}
+        if not all(torch.cuda.can_device_access_peer(local, d) for d in nbrs):
+            exchange_note = f"no peer access from cuda:{local} to {sorted(nbrs)}: NCCL exchange"
+            args.exchange = "nccl"
+        flag = torch.tensor([args.exchange == "nccl"], dtype=torch.int32, device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX)  # every rank takes the same exchange
+        if flag.item():
+            args.exchange = "nccl"
+            exchange_note = exchange_note or "a rank lacks peer access to its neighbours: NCCL exchange"
     if not host_fed:
         from paper_1908_06094_b200.distributed import StripStepper
 
@@ -364,6 +377,7 @@ def run_ours(args):
                                      "one launch per step: boundary-row epilogue stores into the "
                                      "neighbours' halos (CUDA IPC over NVLink), in-kernel step fence"
                                      if args.exchange == "p2p" else "NCCL grouped send/recv"),
+                   **({"exchange_fallback": exchange_note} if exchange_note else {}),
                    "l2": "256 MiB read-only L2 flush before every timed step (outside the events)",
                    "fused_schedule": ("band round robin" if band else "contiguous ranges"),
                    "fused_tile": {"variant": variant, "ti": vi[0].value, "tj": vi[1].value, "kc": vi[2].value,
