@@ -255,6 +255,8 @@ def run_ours(args):
         stepper.step(DT, PIVBZ)
         stepper.swap()
     torch.cuda.synchronize()
+    if not host_fed:
+        stepper.check()  # a broken exchange fails here, not after every timed step has timed out
     barrier()
 
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
