@@ -168,8 +168,12 @@ __device__ inline void wait_both(const int64_t *flags, int64_t value, uint64_t t
 // the shared interface flux k+1 computed once, half the per-unit overhead per point.
 // PEER: the launch stores its strip's boundary rows into the ring neighbours' halo rows
 // (a separate instantiation so the single-GPU kernel carries none of that epilogue)
-template <int TI, int TJ, int KC, int STAGES, int LV, int LP, int OP, bool PEER = false, bool BAND = false>
-__global__ void __launch_bounds__(TI *TJ * LV, 1)
+// WS: warp-specialised -- one extra producer warp issues the TMA loads and each consumer
+// warp releases a stage through an "empty" mbarrier, so the consumer warps are not
+// lock-stepped by a CTA barrier at every unit
+template <int TI, int TJ, int KC, int STAGES, int LV, int LP, int OP, bool PEER = false, bool BAND = false,
+          bool WS = false>
+__global__ void __launch_bounds__(TI *TJ * LV + (WS ? 32 : 0), 1)
     mpdata_fused_kernel(const __grid_constant__ CUtensorMap tm_pd,
                         const __grid_constant__ CUtensorMap tm_vn,
                         const __grid_constant__ CUtensorMap tm_wn,
@@ -178,6 +182,8 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
     using C = FusedCfg<TI, TJ, KC, STAGES, LV, LP>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * C::kStageBytes);
+    uint64_t *empty = bars + STAGES;  // WS: consumer warps release stages here
+    constexpr int kConsumers = TI * TJ * LV;
 
     const int tid = threadIdx.x;
     const int kl = tid % LV;    // level lane inside the chunk
@@ -207,6 +213,8 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
         prefetch_tmap(&tm_wn);
         prefetch_tmap(&tm_rho);
         for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+        if constexpr (WS)
+            for (int s = 0; s < STAGES; ++s) mbar_init(&empty[s], kConsumers / 32);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if constexpr (OP == kComputeProbe) {  // benign operands: no slow-path divisions
@@ -257,7 +265,20 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
             }
         }
     };
-    if (tid == 0) {
+    if constexpr (WS) {
+        if (tid >= kConsumers) {  // the producer warp
+            if (tid == kConsumers && OP != kComputeProbe) {
+                for (int n = 0; n < n_units; ++n) {
+                    const int stage = n % STAGES;
+                    if (n >= STAGES) mbar_wait(&empty[stage], (uint32_t)((n / STAGES - 1) & 1));
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    issue_next(stage);
+                }
+            }
+            __syncthreads();  // matches the consumers' closing barrier
+            return;
+        }
+    } else if (tid == 0) {
         if (OP != kComputeProbe)
             for (int s = 0; s < STAGES - 1 && s < n_units; ++s) issue_next(s);
     }
@@ -279,7 +300,7 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
 
     for (int n = 0; n < n_units; ++n) {
         const int stage = n % STAGES;
-        if (tid == 0 && n + STAGES - 1 < n_units) {
+        if (!WS && tid == 0 && n + STAGES - 1 < n_units) {
             // that stage was released by the __syncthreads() closing unit n-1
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             if (OP != kComputeProbe) issue_next((n + STAGES - 1) % STAGES);
@@ -458,8 +479,14 @@ __global__ void __launch_bounds__(TI *TJ * LV, 1)
                 ++ti;
             }
         }
-        __syncthreads();  // every thread is done with this stage
+        if constexpr (WS) {
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&empty[stage]);
+        } else {
+            __syncthreads();  // every thread is done with this stage
+        }
     }
+    if constexpr (WS) __syncthreads();  // every consumer's stores are issued
     if constexpr (PEER) {
         if (a.done && tid == 0) {  // the last CTA out releases the step into both neighbours
             __threadfence_system();  // this CTA's peer stores are visible system-wide
@@ -486,7 +513,7 @@ struct Variant {
     void *peer_band[2];  // the same with the fused halo-row stores (row strips)
 };
 
-template <int TI, int TJ, int KC, int STAGES, int LV = 16, int LP = 1>
+template <int TI, int TJ, int KC, int STAGES, int LV = 16, int LP = 1, bool WS = false>
 static Variant make_variant() {
     using C = FusedCfg<TI, TJ, KC, STAGES, LV, LP>;
     Variant v;
@@ -494,20 +521,20 @@ static Variant make_variant() {
     v.tj = TJ;
     v.kc = KC;
     v.stages = STAGES;
-    v.threads = C::kThreads;
+    v.threads = C::kThreads + (WS ? 32 : 0);
     v.smem = C::kSmemBytes;
-    v.fn[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND>;
-    v.fn[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED>;
-    v.fn[2] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, kProbeOp>;
-    v.fn[3] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, kComputeProbe>;
-    v.peer[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND, true>;
-    v.peer[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED, true>;
+    v.fn[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND, false, false, WS>;
+    v.fn[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED, false, false, WS>;
+    v.fn[2] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, kProbeOp, false, false, WS>;
+    v.fn[3] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, kComputeProbe, false, false, WS>;
+    v.peer[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND, true, false, WS>;
+    v.peer[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED, true, false, WS>;
     v.band[0] = v.band[1] = v.peer_band[0] = v.peer_band[1] = nullptr;
     if constexpr (LP == 2) {  // the level-pair variants only (the default and its kin)
-        v.band[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND, false, true>;
-        v.band[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED, false, true>;
-        v.peer_band[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND, true, true>;
-        v.peer_band[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED, true, true>;
+        v.band[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND, false, true, WS>;
+        v.band[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED, false, true, WS>;
+        v.peer_band[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND, true, true, WS>;
+        v.peer_band[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED, true, true, WS>;
     }
     return v;
 }
@@ -528,12 +555,14 @@ static Variant *variants(int *count) {
         make_variant<2, 8, 80, 2, 32>(),   // 12: whole 80-level columns, 512 threads
         make_variant<4, 4, 80, 2, 32>(),   // 13: whole 80-level columns, 512 threads
         make_variant<2, 8, 48, 2, 32>(),   // 14: 48-level chunks, 512 threads
-        make_variant<4, 16, 16, 3, 8, 2>(),  // 15 (default): level pairs, 512 threads, 3 x 65.5 KB
+        make_variant<4, 16, 16, 3, 8, 2>(),  // 15: level pairs, 512 threads, 3 x 65.5 KB
         make_variant<4, 8, 16, 3, 8, 2>(),   // 16: level pairs, 256 threads, 2 CTAs / SM
         make_variant<2, 16, 16, 2, 8, 2>(),  // 17: level pairs, 256 threads, 2 CTAs / SM
         make_variant<8, 8, 16, 3, 8, 2>(),   // 18: level pairs, 512 threads, 3 x 63 KB
         make_variant<16, 4, 16, 3, 8, 2>(),  // 19: level pairs, 512 threads, tall tiles
         make_variant<32, 2, 16, 3, 8, 2>(),  // 20: level pairs, 512 threads, taller tiles
+        make_variant<4, 16, 16, 3, 8, 2, true>(),  // 21 (default): variant 15 + a producer warp
+        make_variant<4, 12, 16, 4, 8, 2, true>(),  // 22: producer warp, 384 + 32 threads, 4 x 51.4 KB
     };
     *count = (int)(sizeof(v) / sizeof(v[0]));
     return v;
@@ -547,7 +576,7 @@ static Variant *variants(int *count) {
 // tile is best (279x256x80: 63.6 vs 65.5 us for 16x4).  Otherwise every upper halo is
 // re-read from DRAM (ncu at O1280: 32 % of the step's reads) and the tall 16x4 tile, with
 // two halo rows per 16 instead of per 4, is faster (O1280: 10.06-10.12 vs 10.41-10.47 ms).
-static constexpr int kCompactVariant = 15, kTallVariant = 19;
+static constexpr int kCompactVariant = 21, kTallVariant = 19;
 constexpr int kGraphMinSteps = 4;  // tsg_mpdata_run replays a captured two-step graph from here
 constexpr double kReuseUnits = 8.0;
 static int g_variant = 0;  // 0 = choose per launch (pick_variant)

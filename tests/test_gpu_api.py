@@ -332,9 +332,9 @@ def test_default_fused_variant_follows_the_l2_reuse_rule(cuda_ok):
 
     lib = _lib.lib()
     bench, big = DeviceGrid(279, 256, 80), DeviceGrid(2560, 2576, 137)
-    assert lib.tsg_fused_variant_of(bench.handle, 0, 279) == 15
+    assert lib.tsg_fused_variant_of(bench.handle, 0, 279) == 21  # 4x16, producer warp
     assert lib.tsg_fused_band_of(bench.handle, 0, 279) == 0
-    assert lib.tsg_fused_variant_of(big.handle, 0, 2560) == 15
+    assert lib.tsg_fused_variant_of(big.handle, 0, 2560) == 21
     assert lib.tsg_fused_band_of(big.handle, 0, 2560) == 1
     _lib.call("tsg_set_fused_band", 0)
     try:

@@ -88,8 +88,10 @@ def test_fused_variant_smem_fits_an_sm():
         vals = [ctypes.c_int() for _ in range(6)]
         _lib.check(lib.tsg_fused_variant_info(v, *[ctypes.byref(x) for x in vals]))
         ti, tj, kc, stages, threads, smem = (x.value for x in vals)
-        # LV lanes per vertex: 16 / 32 (a thread per level) or kc / 2 (a thread per level pair)
-        assert threads in (ti * tj * 16, ti * tj * 32, ti * tj * kc // 2) and threads <= 1024 and kc % 16 == 0
+        # LV lanes per vertex: 16 / 32 (a thread per level) or kc / 2 (a thread per level pair),
+        # plus one producer warp in the warp-specialised variants
+        assert threads in (ti * tj * 16, ti * tj * 32, ti * tj * kc // 2, ti * tj * kc // 2 + 32)
+        assert threads <= 1024 and kc % 16 == 0
         stage = sum(-(-b // 128) * 128 for b in ((ti + 2) * (tj + 2) * (kc + 4) * 8,
                                                  (ti + 1) * 3 * (tj + 1) * kc * 8,
                                                  ti * tj * (kc + 2) * 8, ti * tj * kc * 8))
