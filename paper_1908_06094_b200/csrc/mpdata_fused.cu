@@ -275,8 +275,7 @@ __global__ void __launch_bounds__(TI *TJ * LV + (WS ? 32 : 0), 1)
                     issue_next(stage);
                 }
             }
-            __syncthreads();  // matches the consumers' closing barrier
-            return;
+            return;  // nothing after the unit loop involves the producer
         }
     } else if (tid == 0) {
         if (OP != kComputeProbe)
@@ -486,7 +485,8 @@ __global__ void __launch_bounds__(TI *TJ * LV + (WS ? 32 : 0), 1)
             __syncthreads();  // every thread is done with this stage
         }
     }
-    if constexpr (WS) __syncthreads();  // every consumer's stores are issued
+    if constexpr (WS && PEER)  // every consumer's stores are issued (consumer warps only)
+        asm volatile("bar.sync 1, %0;" ::"r"(kConsumers) : "memory");
     if constexpr (PEER) {
         if (a.done && tid == 0) {  // the last CTA out releases the step into both neighbours
             __threadfence_system();  // this CTA's peer stores are visible system-wide
