@@ -187,9 +187,11 @@ int tsg_transport_indirect(const int64_t *e2v, const int64_t *v2e, const double 
                            int nlev, double dt, double pivbz, int flux_op, double *flux,
                            double *fluz, double *div, double *pd_out, tsg_stream s);
 /* Select the fused kernel's tile variant; 0 (the default) chooses per launch: the compact
- * 4x16 tile when the tile above a tile is still in L2 under the contiguous schedule, else
- * the tall 16x4 tile (tsg_fused_variant_of).  Variant 0 in _info = the forced variant, or
- * the compact tile when none is forced. */
+ * 4x16 level-pair tile with a producer warp (variant 21: 512 compute threads + 32) when
+ * the tile above a tile is still in L2 under the contiguous schedule or the band schedule
+ * applies, else the tall 16x4 tile (tsg_fused_variant_of).  Variant 0 in _info = the
+ * forced variant, or the compact tile when none is forced; `threads` counts the producer
+ * warp. */
 int tsg_set_fused_variant(int variant);
 int tsg_fused_variant_info(int variant, int *ti, int *tj, int *kc, int *stages, int *threads,
                            int *smem_bytes);
