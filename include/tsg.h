@@ -57,6 +57,9 @@ enum tsg_grid_flags {
 };
 
 /* ---- errors / version ------------------------------------------------------------ */
+/* No reference counterpart: the reference raises ValueError / IndexError / RuntimeError
+ * directly (topology.py:58-75, connectivity.py:147-158); the Python mirror maps the
+ * status codes back to those exception types with this message. */
 const char *tsg_last_error(void);
 int tsg_abi_version(void);
 
@@ -247,6 +250,8 @@ int64_t tsg_permutation_work_elems(int rows, int cols, int loc);
 int tsg_edge_signs(int rows, int cols, double *out, tsg_stream s);
 
 /* ---- cross-GPU plumbing for the fused exchange (one process per GPU) ------------------ */
+/* No reference counterpart: the reference is single-process (SPEC.md:8 names MPI halo
+ * exchange as the multi-node path); these replace it with NVLink P2P stores and flags. */
 /* Device memory outside any caching allocator (IPC handles need whole allocations). */
 int tsg_malloc(int64_t bytes, void **out);
 int tsg_free(void *ptr);
@@ -268,7 +273,8 @@ int tsg_wait_flags(const int64_t *my_flags, int64_t value, int timeout_ms, int *
 int tsg_total_mass(const tsg_grid *g, const double *pd, const double *dual, double *work,
                    double *out, tsg_stream s);
 /* Counter-hash uniform values in [lo, hi) for every (element, level), halo images
- * included -- on-device synthetic inputs for patches the host cannot hold. */
+ * included -- on-device synthetic inputs for patches the host cannot hold (the reference
+ * draws its inputs with numpy, mpdata.py:51-182, which cfg5 / O1280 does not fit). */
 int tsg_fill_hash(const tsg_grid *g, int loc, int inner, uint64_t seed, double lo, double hi,
                   double *field, tsg_stream s);
 
