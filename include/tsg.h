@@ -58,7 +58,7 @@ enum tsg_grid_flags {
 
 /* ---- errors / version ------------------------------------------------------------ */
 /* No reference counterpart: the reference raises ValueError / IndexError / RuntimeError
- * directly (topology.py:58-75, connectivity.py:147-158); the Python mirror maps the
+ * directly (topology.py:58-75, connectivity.py:94-150); the Python mirror maps the
  * status codes back to those exception types with this message. */
 const char *tsg_last_error(void);
 int tsg_abi_version(void);
