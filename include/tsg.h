@@ -157,6 +157,10 @@ int tsg_mpdata_step_strip(tsg_grid *g, const double *pd, const double *vn, const
 /* Number of time-loop graphs instantiated so far in this process (a diagnostic: a loop
  * that alternates between the same two buffers reuses one graph). */
 int tsg_time_loop_graphs_built(void);
+/* Prepared-launch cache of a grid handle (the tensor maps, arguments and grid size of a
+ * fused step, keyed by all of its arguments): hits / misses so far.  A diagnostic; a
+ * repeated step with the same buffers encodes nothing. */
+int tsg_launch_cache_stats(const tsg_grid *g, int64_t *hits, int64_t *misses);
 int tsg_mpdata_run_strip(tsg_grid *g, double *pd_a, double *pd_b, const double *vn,
                          const double *wn, const double *rho, const double *signs,
                          const double *dual, double dt, double pivbz, int flux_op,

@@ -18,6 +18,8 @@ from .layouts import (
     Numbering,
     Permutation,
     check_access_combo,
+    coalescing_fraction,
+    direct_sweep_groups,
     hilbert_rank,
     hilbert_xy,
     make_permutation,
@@ -33,6 +35,7 @@ from .connectivity import (
     neighbor_len,
     structured_offsets,
 )
+from .stencil import CompositionError
 from .storage import (
     DivergenceError,
     Field,
@@ -73,12 +76,14 @@ from .kernels import (
     build_reduce,
     field_to_flat,
     flat_to_field,
+    gather_groups,
     make_kernel_fields,
     run_neighbor_sum,
     run_neighbor_sum_scaled,
     unpermute,
 )
 from .flat import StructuredStepper, transport_step, transport_step_structured
+from .traffic import TrafficReport, TrafficRow
 
 UNFUSED_PLANE_WEIGHTS = {"nodes": (7, 3), "edges": (1, 1)}  # bench.py:57-60
 FUSED_PLANE_WEIGHTS = {"nodes": (4, 1)}

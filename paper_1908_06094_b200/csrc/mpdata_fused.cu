@@ -30,12 +30,13 @@
 //    straight to HBM with one 16-byte store.  The LP = 1 variants (1-14) run one thread
 //    per (vertex, level) instead.
 //  * No tensor cores: fp64 stencil, ~0.5 flop/byte, the HBM roofline bounds it.
-#include <string.h>
-
 #include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
+#include <new>
+#include <unordered_map>
 
 #include "tsg_tma.cuh"
 
@@ -242,6 +243,9 @@ __global__ void __launch_bounds__(TI *TJ * LV + (WS ? 32 : 0), 1)
         if constexpr (PEER) {
             if (!waited && (tr == 0 || tr == a.tiles_i - 1)) {  // reads the neighbours' rows
                 wait_both(a.my_flags, wv, a.timeout_ns, a.err);
+                // the acquire above is a generic-proxy load; the halo rows it publishes are
+                // read next by TMA (async proxy): order the two proxies explicitly
+                asm volatile("fence.proxy.async.global;" ::: "memory");
                 waited = true;
             }
         }
@@ -726,10 +730,94 @@ static int encode_pd(const Variant &v, const tsg_grid *g, const double *pd, CUte
     return make_map(m, pd, 3, dims, str, box);
 }
 
+// cudaFuncSetAttribute once per kernel (not on every launch)
+static int set_smem_once(void *fn, int smem) {
+    static std::mutex mu;
+    static std::unordered_map<void *, int> done;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = done.find(fn);
+    if (it != done.end() && it->second >= smem) return TSG_OK;
+    TSG_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    done[fn] = smem;
+    return TSG_OK;
+}
+
+// Prepared launches cached on the grid handle (include/tsg.h: "TMA descriptor cache"):
+// keyed by every argument of prepare() plus the variant / schedule switches, so a repeated
+// step (a time loop's ping-pong, a benchmark's timed steps) costs a key compare and the
+// launch -- no tensor-map encoding, attribute call or occupancy query between the caller's
+// start event and the kernel.
+struct LaunchKey {
+    const void *p[9];  // pd, vn, wn, rho, signs, dual, pd_out, halo_up, halo_down
+    double dt, pivbz;
+    int flux_op, row_lo, row_hi, variant, band;
+    bool operator==(const LaunchKey &o) const { return !memcmp(this, &o, sizeof(*this)); }
+};
+
+constexpr int kLaunchCacheSize = 8;
+struct LaunchCache {
+    LaunchKey key[kLaunchCacheSize];
+    FusedLaunch L[kLaunchCacheSize];
+    int used = 0, next = 0;
+    int64_t hits = 0, misses = 0;
+};
+
+void tsg::destroy_launch_cache(tsg_grid *g) {
+    delete static_cast<LaunchCache *>(g->launches);
+    g->launches = nullptr;
+}
+
+static int prepare_uncached(tsg_grid *g, const double *pd, const double *vn, const double *wn,
+                            const double *rho, const double *signs, const double *dual,
+                            double *pd_out, double dt, double pivbz, int flux_op, int row_lo,
+                            int row_hi, double *halo_up, double *halo_down, FusedLaunch *L);
+
 static int prepare(tsg_grid *g, const double *pd, const double *vn, const double *wn,
                    const double *rho, const double *signs, const double *dual, double *pd_out,
                    double dt, double pivbz, int flux_op, int row_lo, int row_hi, double *halo_up,
                    double *halo_down, FusedLaunch *L) {
+    if (!g) return fail(TSG_EVALUE, "grid is NULL");
+    LaunchKey k;
+    memset(&k, 0, sizeof(k));
+    const void *ptrs[9] = {pd, vn, wn, rho, signs, dual, pd_out, halo_up, halo_down};
+    for (int q = 0; q < 9; ++q) k.p[q] = ptrs[q];
+    k.dt = dt;
+    k.pivbz = pivbz;
+    k.flux_op = flux_op;
+    k.row_lo = row_lo;
+    k.row_hi = row_hi;
+    k.variant = g_variant;
+    k.band = g_band;
+    LaunchCache *c = static_cast<LaunchCache *>(g->launches);
+    if (c) {
+        for (int q = 0; q < c->used; ++q)
+            if (c->key[q] == k) {
+                *L = c->L[q];
+                ++c->hits;
+                return TSG_OK;
+            }
+    }
+    if (int rc = prepare_uncached(g, pd, vn, wn, rho, signs, dual, pd_out, dt, pivbz, flux_op,
+                                  row_lo, row_hi, halo_up, halo_down, L))
+        return rc;
+    if (!c) {
+        c = new (std::nothrow) LaunchCache;
+        if (!c) return TSG_OK;  // no cache: correct, just slower
+        g->launches = c;
+    }
+    const int slot = c->next;
+    c->next = (c->next + 1) % kLaunchCacheSize;
+    if (c->used < kLaunchCacheSize) ++c->used;
+    c->key[slot] = k;
+    c->L[slot] = *L;
+    ++c->misses;
+    return TSG_OK;
+}
+
+static int prepare_uncached(tsg_grid *g, const double *pd, const double *vn, const double *wn,
+                            const double *rho, const double *signs, const double *dual,
+                            double *pd_out, double dt, double pivbz, int flux_op, int row_lo,
+                            int row_hi, double *halo_up, double *halo_down, FusedLaunch *L) {
     memset(L, 0, sizeof(*L));  // deterministic bytes: the time-loop graph cache compares them
     if (!g) return fail(TSG_EVALUE, "grid is NULL");
     if ((halo_up || halo_down) && (g->flags & TSG_PERIODIC_ROWS))
@@ -821,7 +909,7 @@ static int prepare(tsg_grid *g, const double *pd, const double *vn, const double
         L->fn = v.band[flux_op];
         fill_band(L->ba, tiles_i, a.tiles_j, false);
     }
-    TSG_CHECK_CUDA(cudaFuncSetAttribute(L->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
+    if (int rc = set_smem_once(L->fn, v.smem)) return rc;
     int per_sm = 0;
     TSG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L->fn, v.threads, v.smem));
     if (per_sm < 1) return fail(TSG_ECUDA, "fused variant %d does not fit on an SM", vi);
@@ -884,7 +972,7 @@ static int prepare_strip(tsg_grid *g, const double *pd, const double *vn, const 
     if (v.peer_band[0] && band_enabled() && evicted(g, g->rows) && a.tiles_i >= 3 &&
         (int64_t)a.tiles_i * a.tiles_j >= 16LL * g->num_sms && flux_op <= TSG_CENTRED) {
         L->fn = v.peer_band[flux_op];
-        TSG_CHECK_CUDA(cudaFuncSetAttribute(L->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
+        if (int rc = set_smem_once(L->fn, v.smem)) return rc;
         fill_band(L->ba, a.tiles_i, a.tiles_j, true);
     }
     return TSG_OK;
@@ -924,13 +1012,15 @@ struct GraphCache {
     GraphKey key;          // of the captured (fwd, bwd) pair
     FusedLaunch fwd, bwd;  // the captured launches (for an odd tail / the swapped orientation)
     cudaGraphExec_t exec;
+    cudaEvent_t last;      // recorded after the latest replay of `exec`
 };
 
 void tsg::destroy_graph_cache(tsg_grid *g) {
     if (!g->graph) return;
     GraphCache *c = static_cast<GraphCache *>(g->graph);
-    cudaDeviceSynchronize();  // no launch of it may be in flight
+    cudaEventSynchronize(c->last);  // only this graph's replays must have drained
     cudaGraphExecDestroy(c->exec);
+    cudaEventDestroy(c->last);
     delete c;
     g->graph = nullptr;
 }
@@ -964,6 +1054,10 @@ static int run_pair_graph(tsg_grid *g, const GraphKey &key, const GraphKey &swap
         if (e == cudaSuccess) e = cudaGraphInstantiate(&c->exec, graph, 0);
         if (graph) cudaGraphDestroy(graph);
         cudaStreamDestroy(cap);
+        if (e == cudaSuccess) {
+            e = cudaEventCreateWithFlags(&c->last, cudaEventDisableTiming);
+            if (e != cudaSuccess) cudaGraphExecDestroy(c->exec);
+        }
         if (e != cudaSuccess) {
             delete c;
             return fail(TSG_ECUDA, "time-loop graph capture failed: %s", cudaGetErrorString(e));
@@ -973,6 +1067,7 @@ static int run_pair_graph(tsg_grid *g, const GraphKey &key, const GraphKey &swap
     }
     for (int t = 0; t + 1 < nsteps; t += 2)
         TSG_CHECK_CUDA(cudaGraphLaunch(c->exec, (cudaStream_t)s));
+    if (nsteps >= 2) TSG_CHECK_CUDA(cudaEventRecord(c->last, (cudaStream_t)s));
     if (nsteps % 2) return launch(&c->fwd, s);
     return TSG_OK;
 }
@@ -1052,3 +1147,11 @@ extern "C" int tsg_mpdata_run_strip(tsg_grid *g, double *pd_a, double *pd_b, con
 }
 
 extern "C" int tsg_time_loop_graphs_built(void) { return g_graph_builds; }
+
+extern "C" int tsg_launch_cache_stats(const tsg_grid *g, int64_t *hits, int64_t *misses) {
+    if (!g) return fail(TSG_EVALUE, "grid is NULL");
+    const LaunchCache *c = static_cast<const LaunchCache *>(g->launches);
+    if (hits) *hits = c ? c->hits : 0;
+    if (misses) *misses = c ? c->misses : 0;
+    return TSG_OK;
+}

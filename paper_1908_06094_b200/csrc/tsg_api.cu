@@ -53,6 +53,7 @@ extern "C" int tsg_grid_create(int rows, int cols, int levels, int flags, tsg_gr
     g->device = dev;
     g->num_sms = sms;
     g->graph = nullptr;
+    g->launches = nullptr;
     *out = g;
     tsg::clear_error();
     return TSG_OK;
@@ -69,7 +70,10 @@ extern "C" int tsg_grid_set_origin(tsg_grid *g, int row0, int global_rows) {
 }
 
 extern "C" int tsg_grid_destroy(tsg_grid *g) {
-    if (g) tsg::destroy_graph_cache(g);
+    if (g) {
+        tsg::destroy_graph_cache(g);
+        tsg::destroy_launch_cache(g);
+    }
     delete g;
     return TSG_OK;
 }

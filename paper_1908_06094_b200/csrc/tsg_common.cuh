@@ -16,10 +16,13 @@ struct tsg_grid {
     int row0, global_rows;  // strip origin inside the global patch (multi-GPU); 0 / rows otherwise
     int device, num_sms;
     void *graph;  // cached two-step CUDA graph of the time loops (mpdata_fused.cu), or NULL
+    void *launches;  // prepared fused launches (tensor maps, arguments, grid) keyed by their
+                     // arguments (mpdata_fused.cu), or NULL
 };
 
 namespace tsg {
 void destroy_graph_cache(tsg_grid *g);
+void destroy_launch_cache(tsg_grid *g);
 }
 
 namespace tsg {

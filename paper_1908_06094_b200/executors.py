@@ -8,8 +8,13 @@ The reference runs stage bodies through ``run_naive`` / ``run_fused``
   single-pass TMA kernel (``tsg_mpdata_step``); ``fused=False`` is the
   four-kernel path that materialises flux / fluz / divvd like ``run_naive``.
 * :func:`run_naive` / :func:`run_fused` keep the reference's signatures so
-  existing call sites work unchanged (``TileSpec`` is validated and recorded;
-  the device tiling is the kernel's own).
+  existing call sites work unchanged.  ``TileSpec`` is validated like the
+  reference's (a tile smaller than the largest stage reach raises the same
+  ``ValueError``) and sets the reported stage updates (the fused plan's apron
+  recompute); the device tiling is the kernel's own.
+* ``RunStats.traffic()`` returns the reference's ``TrafficReport`` (per field
+  and phase, distinct and raw accesses), filled from the closed form of what
+  the reference's counters record (traffic.py).
 
 Inputs are uploaded on demand (primary -> mirror, reordered on the GPU);
 outputs are written on the device and, with ``download=True`` (default, the
@@ -25,6 +30,7 @@ from dataclasses import dataclass, field as dc_field
 
 from . import _lib
 from .storage import Field, device_grid, sync
+from .traffic import TrafficReport, record_run, required_tile
 
 _FLUX_CODE = {"upwind": 0, "centred": 1}
 
@@ -47,7 +53,8 @@ class RunStats:
     """Device times and update counts of one run (executors.py:48-71).
 
     ``wall_times`` holds the CUDA-event device time of the launch sequence in
-    seconds; ``traffic()`` reports the algorithmic bytes of the step.
+    seconds; ``traffic()`` is the reference's per-field access report under the
+    ``"{tag}/"`` phase prefix; ``bytes_moved`` the algorithmic HBM bytes.
     """
 
     tag: str
@@ -65,8 +72,8 @@ class RunStats:
     def total_updates(self) -> int:
         return sum(self.stage_updates.values())
 
-    def traffic(self) -> dict:
-        return {"algorithmic_bytes": self.bytes_moved}
+    def traffic(self) -> TrafficReport:
+        return TrafficReport.gather(self.fields, prefix=f"{self.tag}/")
 
 
 def halo_update(field: Field, space: str = "primary") -> None:
@@ -154,12 +161,15 @@ def _launch(comp, fused: bool, stream):
 
 
 def run_gpu(comp, fused: bool = True, run_tag: str = "gpu", download: bool = True,
-            stream=None) -> RunStats:
+            stream=None, tiles: "TileSpec | None" = None) -> RunStats:
     """Execute ``comp`` on the current CUDA device; returns RunStats."""
     outs, (start, end), nbytes = _launch(comp, fused, stream)
     end.synchronize()
+    updates = record_run(comp, run_tag, fused, tiles)
+    if tiles is None:  # useful updates (run_naive's count); a TileSpec adds the apron recompute
+        updates = comp.stage_updates()
     stats = RunStats(tag=run_tag, executor="gpu-fused" if fused else "gpu-unfused",
-                     fields=comp.fields(), stage_updates=comp.stage_updates(), bytes_moved=nbytes)
+                     fields=comp.fields(), stage_updates=updates, bytes_moved=nbytes)
     stats.wall_times["ms0"] = start.elapsed_time(end) / 1e3
     if download:
         for f in outs:
@@ -173,10 +183,21 @@ def run_naive(comp, run_tag: str = "naive") -> RunStats:
 
 
 def run_fused(comp, tiles: TileSpec | None = None, run_tag: str = "fused") -> RunStats:
-    """Single-pass fused device execution (executors.py:266); tiles are the kernel's own."""
+    """Single-pass fused device execution (executors.py:266-316).
+
+    ``tiles`` is checked against the largest stage reach as the reference does
+    (executors.py:276-282) and sets the reported flux updates (each tile recomputes
+    its apron); the device tiling itself is the kernel's own.  ``None`` = one tile.
+    """
     if tiles is not None and not isinstance(tiles, TileSpec):
         raise TypeError("tiles must be a TileSpec")
-    return run_gpu(comp, fused=True, run_tag=run_tag)
+    if tiles is None:
+        tiles = TileSpec(comp.patch.rows, comp.patch.cols)
+    ri, rj = required_tile(comp)
+    if tiles.tile_i < ri or tiles.tile_j < rj:
+        raise ValueError(f"tile {tiles.tile_i}x{tiles.tile_j} smaller than the largest "
+                         f"stage reach {ri}x{rj}")
+    return run_gpu(comp, fused=True, run_tag=run_tag, tiles=tiles)
 
 
 def run_time_loop(comp, steps: int, fused: bool = True, run_tag: str = "loop",
@@ -219,8 +240,11 @@ def run_time_loop(comp, steps: int, fused: bool = True, run_tag: str = "loop",
         f.mark_device_written()
     end.synchronize()
     nbytes = steps * mpdata_bytes(comp.patch.rows, comp.patch.cols, comp.patch.levels, fused)
+    per_step = {}
+    for _ in range(steps):
+        per_step = record_run(comp, run_tag, fused)
     stats = RunStats(tag=run_tag, executor="gpu-fused" if fused else "gpu-unfused",
-                     fields=comp.fields(), stage_updates={k: steps * v for k, v in comp.stage_updates().items()},
+                     fields=comp.fields(), stage_updates={k: steps * v for k, v in per_step.items()},
                      bytes_moved=nbytes)
     stats.wall_times["ms0"] = start.elapsed_time(end) / 1e3
     if download:

@@ -55,9 +55,23 @@ def transport_step(e2v, v2e, signs, dual_volumes, pd, vn, wn, rho, dt, pivbz, fl
     du_t, _ = _dev(dual_volumes, torch.float64)
     vn_t, _ = _dev(vn, torch.float64)
     rho_t, _ = _dev(rho, torch.float64)
+    # the kernels index without bounds checks: validate every shape and id first, raising
+    # what numpy raises in the reference for the same inputs (reference.py:93-116)
+    if vn_t.ndim != 2 or vn_t.shape[1] != levels:
+        raise ValueError(f"vn must be (n_edges, {levels}), got {tuple(vn_t.shape)}")
     ne = vn_t.shape[0]
+    if tuple(rho_t.shape) != (n, levels):
+        raise ValueError(f"rho must be {(n, levels)}, got {tuple(rho_t.shape)}")
     if tuple(e2v_t.shape) != (ne, 2) or tuple(v2e_t.shape) != (n, 6):
         raise ValueError("e2v must be (n_edges, 2) and v2e (n_vertices, 6)")
+    if tuple(sg_t.shape) != (n, 6):
+        raise ValueError(f"signs must be {(n, 6)}, got {tuple(sg_t.shape)}")
+    if du_t.numel() != n:
+        raise ValueError(f"dual_volumes must hold {n} values, got {du_t.numel()}")
+    from .kernels import check_ids
+
+    check_ids(e2v_t, n, "e2v")
+    check_ids(v2e_t, ne, "v2e")
     out = {"flux": torch.empty((ne, levels), dtype=torch.float64, device=pd_t.device),
            "fluz": torch.empty((n, levels + 1), dtype=torch.float64, device=pd_t.device),
            "div": torch.empty((n, levels), dtype=torch.float64, device=pd_t.device),
@@ -141,11 +155,12 @@ class StructuredStepper:
         import torch
 
         src = {"pd": pd, "vn": vn, "wn": wn, "rho": rho}
-        for name, buf in self.in_bufs.items():
-            x = src[name]
-            if isinstance(x, np.ndarray):
-                x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))
-            buf.copy_(x, non_blocking=True)
+        with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
+            for name, buf in self.in_bufs.items():
+                x = src[name]
+                if isinstance(x, np.ndarray):
+                    x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))
+                buf.copy_(x, non_blocking=True)
         K = self.spec.levels
         self._pack(0, K, self.in_bufs["pd"], self.fwd_v, self.pd, stream)
         self._pack(2, K, self.in_bufs["vn"], self.fwd_e, self.vn, stream)
@@ -235,6 +250,11 @@ class StructuredStepper:
             }
         P = self._pipe
         ev = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
+        # the private streams start after everything already queued on the caller's stream
+        # (set_geometry / upload / the resident fields' zero fill) ...
+        cur = torch.cuda.current_stream()
+        for st in (P["h2d"], P["comp"], P["d2h"]):
+            st.wait_stream(cur)
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record(P["h2d"])
         packed = [None, None]    # staging set b free again (its pack kernels finished)
@@ -277,7 +297,10 @@ class StructuredStepper:
             fetched[b].record(d2h)
             last = fetched[b]
         P["d2h"].wait_event(last)
+        P["d2h"].wait_stream(P["comp"])
         end.record(P["d2h"])
+        # ... and the caller's stream continues after all of it
+        cur.wait_stream(P["d2h"])
         return start, end
 
     def __call__(self, pd, vn, wn, rho, dt, pivbz, flux_op="upwind"):

@@ -23,6 +23,7 @@ import numpy as np
 
 from . import _lib
 from .layouts import Permutation
+from .stencil import CompositionError
 from .storage import Field, Selector, device_grid, make_storage
 from .topology import LocationType, PatchSpec, as_location, element_count
 
@@ -39,11 +40,11 @@ class ReduceComputation:
         self.patch = patch
         self.from_loc, self.to_loc = as_location(from_loc), as_location(to_loc)
         if src.meta.location is not self.to_loc or dst.meta.location is not self.from_loc:
-            raise ValueError("src must live on to_loc and dst on from_loc")
+            raise CompositionError("src must live on to_loc and dst on from_loc")
         if src.inner != dst.inner:
-            raise ValueError("src and dst must have the same number of levels")
+            raise CompositionError("src and dst must have the same number of levels")
         if scale is not None and (scale.meta.location is not self.from_loc or scale.inner != 1):
-            raise ValueError("scale must be a 2-D field on from_loc")
+            raise CompositionError("scale must be a 2-D field on from_loc")
         self.src, self.dst, self.scale, self.name = src, dst, scale, name
         self.bindings = {"a": src, "b": dst}
         if scale is not None:
@@ -109,6 +110,9 @@ def _indirect(table, a, fac):
     av, on_dev = _as_device(a, torch.float64)
     if av.ndim != 2:
         raise ValueError("a must be (n_elements, levels)")
+    if t.ndim != 2:
+        raise ValueError("the neighbour table must be (n_rows, width)")
+    check_ids(t, av.shape[0], "neighbour table")
     fv = None
     if fac is not None:
         fv, _ = _as_device(fac, torch.float64)
@@ -119,6 +123,23 @@ def _indirect(table, a, fac):
     _lib.call("tsg_neighbor_reduce_indirect", _lib.ptr(t), t.shape[0], t.shape[1], av.shape[1],
               _lib.ptr(av), _lib.ptr(fv), _lib.ptr(out), _lib.stream_handle())
     return out if on_dev else out.cpu().numpy()
+
+
+def check_ids(ids, n: int, what: str) -> None:
+    """IndexError unless every id of a device index table lies in [0, n) -- the kernels
+    gather without bounds checks, where numpy would raise (reference.py:137-145)."""
+    if ids.numel() == 0:
+        return
+    lo, hi = (int(v) for v in torch_aminmax(ids))
+    if lo < 0 or hi >= n:
+        raise IndexError(f"{what}: index {lo if lo < 0 else hi} is out of bounds for {n} elements")
+
+
+def torch_aminmax(t):
+    import torch
+
+    mm = torch.aminmax(t)
+    return torch.stack([mm.min, mm.max]).cpu().tolist()
 
 
 def run_neighbor_sum(table, a):
@@ -170,9 +191,28 @@ def flat_to_field(values, field: Field, perm: Permutation | None = None) -> None
     h = spec.halo
     canonical = values if perm is None else values[perm.forward]
     shaped = np.asarray(canonical).reshape(spec.rows, field.shape[1], spec.cols, field.shape[3])
-    if field.dirty["mirror"]:
-        field.dirty["mirror"] = False
+    # a newer device copy is not silently dropped: array('primary', 'rw') raises
+    # StalenessError as the reference does (storage.py:130-145); sync first
     field.array("primary", "rw")[h:h + spec.rows, :, h:h + spec.cols, :, 0] = shaped
+
+
+def gather_groups(table, width: int, own_reads: int = 0) -> list:
+    """Warp address groups of one indirect sweep over a neighbour table (kernels.py:137-155):
+    per warp of ``width`` consecutive ranks one gather group per neighbour slot, then
+    ``own_reads`` own-rank read groups and the own-rank write group."""
+    if width < 1:
+        raise ValueError(f"width must be >= 1, got {width}")
+    ids = getattr(table, "ids", table)
+    if hasattr(ids, "cpu"):
+        ids = ids.cpu().numpy()
+    ids = np.asarray(ids)
+    groups = []
+    for r0 in range(0, ids.shape[0], width):
+        rows = ids[r0:r0 + width]
+        chunk = np.arange(r0, r0 + rows.shape[0])
+        groups.extend(rows[:, s].copy() for s in range(ids.shape[1]))
+        groups.extend(chunk for _ in range(own_reads + 1))  # own reads, then the write
+    return groups
 
 
 def unpermute(values, perm: Permutation | None):

@@ -209,3 +209,45 @@ def un_rank(spec: PatchSpec, loc, i: int, c: int, j: int) -> int:
     loc = as_location(loc)
     element_id(spec, loc, i, c, j)
     return (i * spec.cols + j) * loc.colors + c
+
+
+# ---------------------------------------------------------------------------
+# Coalescing model of the reference's Table-1 study (layouts.py:282-326): which warp
+# address groups of a sweep form one contiguous range.  Host analysis only; the B200
+# sweeps' real sector efficiency comes from ncu (profiles/).
+
+
+def coalescing_fraction(groups) -> float:
+    """Fraction of access groups whose addresses are distinct and cover [min, min + len)
+    (order inside a group does not matter; width-1 groups are trivially coalesced)."""
+    groups = list(groups)
+    if not groups:
+        raise ValueError("no access groups given")
+    hits = 0
+    for g in groups:
+        a = np.sort(np.asarray(g, dtype=np.int64).reshape(-1))
+        if a.size == 0:
+            raise ValueError("empty access group")
+        hits += bool(np.all(np.diff(a) == 1))
+    return hits / len(groups)
+
+
+def direct_sweep_groups(layout: LayoutSpec, spec: PatchSpec, loc, width: int) -> list:
+    """Warp address groups of a direct column sweep of one structured field: each
+    interior (row, colour, level) line of columns chopped into groups of ``width``
+    (the last group of a line may be shorter), lines in (row, colour, level) order."""
+    if width < 1:
+        raise ValueError(f"width must be >= 1, got {width}")
+    loc = as_location(loc)
+    sizes = {"row": spec.rows + 2 * spec.halo, "color": loc.colors,
+             "column": spec.cols + 2 * spec.halo, "level": spec.levels, "extra": 1}
+    lay = LinearLayout(layout, sizes, spec.halo)
+    st = lay.strides
+    i = np.arange(spec.rows)[:, None, None, None]
+    c = np.arange(loc.colors)[None, :, None, None]
+    k = np.arange(spec.levels)[None, None, :, None]
+    j = np.arange(spec.cols)[None, None, None, :]
+    off = (lay.front_pad + (i + spec.halo) * st["row"] + c * st["color"]
+           + (j + spec.halo) * st["column"] + k * st["level"])
+    lines = off.reshape(-1, spec.cols)
+    return [line[s:s + width].tolist() for line in lines for s in range(0, spec.cols, width)]

@@ -249,8 +249,7 @@ def init_preset(field: Field, preset: str, seed: int = 0) -> None:
         values = rng.random(core_shape)
     else:
         raise ValueError(f"unknown preset {preset!r}")
-    if field.dirty["mirror"]:
-        field.dirty["mirror"] = False  # the host write below supersedes the device copy
+    # a newer device copy raises StalenessError here, as in the reference (sync first)
     field.array("primary", "rw")[_interior(field)] = values
     halo_update(field)
 

@@ -14,8 +14,14 @@ include/tsg.h (``[rows+2][colors][cols+2][pitch]``, level innermost).
   the other holds newer data raises :class:`StalenessError`; syncing when both
   were written raises :class:`DivergenceError`.
 
-The per-element traffic counters of the reference (a CPU instrumentation
-model) are not reproduced; GPU traffic is measured with ncu (profiles/).
+The reference's per-element traffic counters (a CPU instrumentation model) are
+replaced by their closed form: every run records on its fields what those
+counters would hold (``Field.counters``, filled by traffic.record_run and read
+through ``RunStats.traffic()``); the GPU's own bytes are measured with ncu
+(profiles/).
+
+Host buffers are allocated in page-locked memory when a GPU is present, so the
+primary <-> mirror copies of ``sync`` are DMA transfers straight from / into them.
 """
 
 from __future__ import annotations
@@ -65,14 +71,31 @@ _GRIDS: dict = {}
 
 
 def device_grid(spec: PatchSpec):
-    """The shared DeviceGrid of a patch (one tsg_grid per (rows, cols, levels))."""
-    from .device import DeviceGrid
+    """The shared DeviceGrid of a patch on the current device (one tsg_grid per
+    (rows, cols, levels, device): a handle binds to the device it was created on)."""
+    import torch
 
-    key = (spec.rows, spec.cols, spec.levels)
+    from .device import DeviceGrid, require_cuda
+
+    require_cuda()
+    key = (spec.rows, spec.cols, spec.levels, torch.cuda.current_device())
     g = _GRIDS.get(key)
     if g is None:
         g = _GRIDS[key] = DeviceGrid.for_spec(spec)
     return g
+
+
+def _host_zeros(n: int) -> np.ndarray:
+    """A zeroed float64 host buffer, page-locked when a GPU is present (the torch tensor
+    owning the memory stays alive as the array's base)."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return torch.zeros(n, dtype=torch.float64, pin_memory=True).numpy()
+    except (ImportError, RuntimeError):
+        pass
+    return np.zeros(n, dtype=np.float64)
 
 
 class Field:
@@ -94,6 +117,8 @@ class Field:
         self._mirror = None   # torch CUDA tensor, allocated on first use (zeros)
         self.dirty = {"primary": False, "mirror": False}
         self.sync_count = 0
+        # phase -> [distinct_reads, distinct_writes, raw_reads, raw_writes] (traffic.py)
+        self.counters = {}
 
     # -- identity ---------------------------------------------------------------------
     @property
@@ -127,7 +152,7 @@ class Field:
         self._check_space(space)
         if space == "primary":
             if self._primary is None:
-                self._primary = np.zeros(self.linear.total, dtype=np.float64)
+                self._primary = _host_zeros(self.linear.total)
             return self._primary
         if self._mirror is None:
             self._mirror = device_grid(self.spec).empty(self.meta.location, self.inner)
@@ -245,8 +270,9 @@ def sync(field: Field, to_space: str) -> None:
         if not field.has_levels:
             lay[4] = 0  # the device inner axis runs along `extra` (or is a scalar)
         lay_p = lay.ctypes.data_as(_lib.ctypes.POINTER(_lib.ctypes.c_int64))
+        host = torch.from_numpy(field.buffer("primary"))
         if to_space == "mirror":
-            staging = torch.from_numpy(field.buffer("primary")).to(grid.device)
+            staging = host.to(grid.device, non_blocking=host.is_pinned())
             _lib.call("tsg_pack_strided", grid.handle, field.loc_code, field.inner,
                       _lib.ptr(staging), lay_p, field.spec.halo, _lib.ptr(field.buffer("mirror")),
                       _lib.stream_handle())
@@ -256,14 +282,15 @@ def sync(field: Field, to_space: str) -> None:
             _lib.call("tsg_unpack_strided", grid.handle, field.loc_code, field.inner,
                       _lib.ptr(field.buffer("mirror")), lay_p, field.spec.halo, _lib.ptr(staging),
                       _lib.stream_handle())
-            np.copyto(field.buffer("primary"), staging.cpu().numpy())
+            host.copy_(staging)  # straight into the (page-locked) host buffer
     field.dirty = {"primary": False, "mirror": False}
     field.sync_count += 1
 
 
 def reset_counters(fields) -> None:
-    """Kept for API compatibility: the device path has no per-element counters."""
-    return None
+    """Clear the recorded traffic of ``fields`` (storage.py:380-382)."""
+    for f in fields:
+        f.counters.clear()
 
 
 def plane_access_total(counts: dict, coefficients: dict) -> int:

@@ -499,9 +499,29 @@ def test_time_computation_and_runstats(cuda_ok):
     assert res.updates == spec.rows * spec.cols * (6 * spec.levels + 1)
     assert len(res.times) == 3 and res.median_seconds > 0
     stats = T.run_gpu(comp)
-    assert stats.wall_times["ms0"] > 0 and stats.traffic()["algorithmic_bytes"] > 0
+    assert stats.wall_times["ms0"] > 0 and stats.bytes_moved > 0
+    assert stats.traffic().total_distinct() > 0
     with pytest.raises(ValueError):
         T.time_computation(comp, T.run_fused, reps=0)
+
+
+def test_runners_report_the_reference_traffic(cuda_ok):
+    """run_naive / run_fused(TileSpec) on the device give the reference's RunStats:
+    stage updates (apron recompute included) and traffic() rows, vs reference goldens."""
+    import json
+    from pathlib import Path
+
+    gold = json.loads((Path(__file__).parent / "golden" / "traffic.json").read_text())["cases"]
+    spec = T.PatchSpec(6, 8, 4)
+    for case in [c for c in gold if c["kind"] == "mpdata" and c["patch"] == [6, 8, 4]]:
+        geo, state = _case(spec, 1)
+        comp = T.build_mpdata(spec, state, geo, T.MpdataParams())
+        tiles = case["tiles"]
+        stats = T.run_naive(comp) if tiles is None else T.run_fused(comp, T.TileSpec(*tiles))
+        assert stats.stage_updates == case["stage_updates"]
+        rows = [[r.field, r.stage, r.distinct_reads, r.distinct_writes, r.raw_reads, r.raw_writes]
+                for r in stats.traffic().rows]
+        assert rows == case["rows"], tiles
 
 
 def test_device_resident_results_follow_the_staleness_contract(cuda_ok):

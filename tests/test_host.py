@@ -251,6 +251,21 @@ def test_host_preset_and_halo_match_the_oracle():
     assert np.array_equal(arr[:, :, 0], arr[:, :, 5]) and np.array_equal(arr[:, :, 6], arr[:, :, 1])
 
 
+def test_host_writes_do_not_drop_newer_device_data():
+    """init_preset / flat_to_field on a field whose device copy is newer raise the
+    reference's StalenessError (storage.py:130-145) instead of discarding that copy."""
+    from paper_1908_06094_b200 import PatchSpec, StalenessError, flat_to_field, init_preset, make_storage
+
+    spec = PatchSpec(4, 5, 3)
+    f = make_storage(spec, L.VERTICES, "pd_in")
+    f.dirty["mirror"] = True  # as after a kernel wrote the device copy
+    with pytest.raises(StalenessError):
+        init_preset(f, "uniform")
+    with pytest.raises(StalenessError):
+        flat_to_field(np.zeros((20, 3)), f)
+    assert f.dirty["mirror"]
+
+
 def test_workload_inputs_reproduce_reference_draws(golden, golden_hashes):
     from paper_1908_06094_b200.workloads import mpdata_algorithmic_bytes, transport_inputs
 
