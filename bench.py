@@ -10,21 +10,28 @@ inputs as the reference's ``_transport_setup`` (gaussian-bump density,
 U[-0.5,0.5) velocities, rho = 1, uniform geometry, dt = 0.1, pivbz = 1).
 
 * value: grid-point updates/s (V*K per step / device time), inputs resident in
-  HBM; each timed step is bracketed by CUDA events on the launching stream and
-  preceded (outside the events) by a 256 MiB L2 flush, so no step reads the
-  previous step's data from L2.
-* e2e: the same metric through the public flat-array API (StructuredStepper)
-  with pinned host buffers, as the reference's time loop runs it (bench.py:398-403:
-  vn / wn / rho fixed, resident like model weights): per step H2D of the density
-  state pd, on-GPU reorder into the structured layout, fused step, reorder back,
-  D2H of pd_out.  ``e2e_all_inputs`` is the flat oracle call pattern
-  (reference.py:93-116) instead: H2D of pd/vn/wn/rho every step.
+  HBM, every rank stepping its 279-row strip of a (279*N) x 256 x 80 patch
+  through ``StripStepper`` (N = 1: the periodic patch; N > 1: row strips with
+  the per-step halo exchange) -- the same code path and the same per-strip
+  inputs at every N (weak scaling).  Each timed step is bracketed by CUDA events
+  on the launching stream, preceded (outside the events) by a 256 MiB L2 flush
+  and a short device sleep that keeps the host's launches ahead of the GPU.
+* o1280_strong: configs[4], the 2560 x 2576 x 137 patch cut into N strips
+  through the same StripStepper path (on-device counter-hash inputs), for the
+  strong-scaling efficiency T1 / (N * T_N) against the N = 1 run's record.
+* e2e (N = 1): independent host-fed steps through the flat-array API
+  (StructuredStepper.run_pipelined): per step H2D of pd from pinned memory,
+  reorder, fused step, reorder, D2H of pd_out, overlapped across steps.
+  ``e2e_all_inputs``: the same with every input (pd / vn / wn / rho) copied per
+  step.  ``e2e_time_loop``: the reference's dependent loop (bench.py:398-403):
+  ``_copy_core(pd_out, pd_in)`` on the host Fields, then ``run_fused(comp,
+  TileSpec)`` -- no overlap possible, step n+1 consumes step n's output.
 * roofline: algorithmic bytes B_comp per step / average step time, against
   the measured HBM copy bandwidth (MEASURED_PEAKS.json).
 * cpu_baseline / --impl reference: the reference algorithm restated in C
-  (oracle/c, bitwise equal to the reference, OpenMP over all host cores).
-* N > 1: weak scaling, one 279-row strip per rank of a (279*N) x 256 x 80
-  patch, row-strip decomposition with a per-step halo exchange (NCCL).
+  (oracle/c, bitwise equal to the reference, OpenMP over all host cores),
+  median step of the same sampling protocol in both arms; the reference arm also
+  times the reference package itself (``run_fused``, baseline/_ref) when installed.
 """
 
 from __future__ import annotations
@@ -32,6 +39,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -57,8 +65,7 @@ WORKLOADS = {
                   label="MPDATA full step, O1280-class periodic patch 2560x2576x137 "
                         "(6,594,560 vertices), row strips across GPUs, fp64"),
 }
-ROWS, COLS, LEVELS = 279, 256, 80
-WORKLOAD = WORKLOADS["cfg3"]["label"]
+SLEEP_CYCLES = 200_000  # ~100 us at 1.965 GHz: the host enqueues flush + events + step meanwhile
 
 
 def _peaks():
@@ -69,8 +76,20 @@ def _peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def workload_config(w: dict, world: int) -> dict:
+    """The ``config`` both arms print for one workload at N ranks (identical dicts)."""
+    rows = w["rows"] * world if w["scaling"] == "weak" else w["rows"]
+    return {"workload": w["label"], "rows": rows, "cols": w["cols"], "levels": w["levels"]}
+
+
+def step_stats(ms: list) -> dict:
+    s = sorted(ms)
+    return {"min": s[0], "median": statistics.median(s), "p90": s[min(len(s) - 1, int(0.9 * len(s)))],
+            "max": s[-1], "mean": sum(s) / len(s), "n": len(s)}
+
+
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled while the GPU works."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -126,11 +145,14 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline (the reference algorithm restated in C; test/baseline infrastructure)
+# CPU baselines (the reference algorithm restated in C; test/baseline infrastructure)
 
 
-def cpu_reference_steps(steps: int, warmup: int, budget_s: float | None = None, rows=ROWS,
-                        cols=COLS, levels=LEVELS):
+def cpu_port_sample(rows: int, cols: int, levels: int, warmup: int, steps: int | None = None,
+                    budget_s: float | None = None):
+    """Step times of the C port on every host core: ``warmup`` untimed steps, then
+    ``steps`` timed ones or as many as fit in ``budget_s`` (at least 3).  Both arms use
+    this and report the median."""
     from oracle import c_oracle
     from oracle import tsg_oracle as O
 
@@ -149,37 +171,75 @@ def cpu_reference_steps(steps: int, warmup: int, budget_s: float | None = None, 
         t0 = time.perf_counter()
         out = c_oracle.transport_step(*args, out=out)
         times.append(time.perf_counter() - t0)
-        if budget_s is None and len(times) >= steps:
+        if steps is not None and len(times) >= steps:
             break
-        if budget_s is not None and (time.perf_counter() - t_begin > budget_s and len(times) >= 3):
+        if budget_s is not None and time.perf_counter() - t_begin > budget_s and len(times) >= 3:
             break
     return times, c_oracle.threads()
 
 
+def cpu_record(w: dict, times, threads) -> dict:
+    r, c, k = w["cpu_rows"], w["cols"], w["levels"]
+    t = statistics.median(times)
+    part = "" if r == w["rows"] else f" (1/{w['rows'] // r} of the per-job patch; updates/s is size-independent)"
+    return {"value": r * c * k / t, "unit": UNIT, "cores": threads, "kind": "port",
+            "ms_per_step": t * 1e3,
+            "sample": f"{r}x{c}x{k} periodic patch{part}, median of {len(times)} steps, "
+                      "reference.transport_step restated in C (oracle/c), OpenMP"}
+
+
+def reference_python_record(w: dict, reps: int) -> dict | None:
+    """The reference package itself (baseline/_ref, unmodified): its fastest CPU path,
+    ``run_fused(comp, TileSpec(R, C, 1))`` via its own ``time_computation`` (median), on
+    ``_transport_setup`` inputs (bench.py:293-303, :386-397)."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "tristencil").is_dir():
+        return None
+    sys.path.insert(0, str(ref))
+    try:
+        from tristencil import mpdata as rmp
+        from tristencil.bench import BenchConfig, _transport_setup
+        from tristencil.executors import TileSpec, time_computation, run_fused
+    finally:
+        sys.path.remove(str(ref))
+    r, c, k = w["cpu_rows"], w["cols"], w["levels"]
+    cfg = BenchConfig(rows=r, cols=c, levels=k, tile_i=r, tile_j=c, workers=1)
+    spec = cfg.patch()
+    state, geo, params = _transport_setup(cfg, spec)
+    comp = rmp.build_mpdata(spec, state, geo, params)
+    tiles = TileSpec(r, c, 1)
+    timing = time_computation(comp, lambda cc: run_fused(cc, tiles), reps=reps, warmup=1)
+    return {"value": r * c * k / timing.median_seconds, "unit": UNIT, "cores": 1,
+            "kind": "reference-python", "ms_per_step": timing.median_seconds * 1e3,
+            "reference_updates_per_second": 1.0 / timing.seconds_per_update,
+            "sample": f"{r}x{c}x{k} patch, tristencil.run_fused(comp, TileSpec({r}, {c}, 1)) "
+                      f"(its fastest path), median of {reps} via its time_computation"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     w = WORKLOADS[args.workload]
-    r, c, k = w["cpu_rows"], w["cols"], w["levels"]
-    steps = args.steps if args.workload == "cfg3" else min(args.steps, 2)
-    times, threads = cpu_reference_steps(steps, min(args.warmup, 1 if args.workload != "cfg3" else args.warmup),
-                                         rows=r, cols=c, levels=k)
-    t = sum(times) / len(times)
-    value = r * c * k / t
-    sample = (f"full {r}x{c}x{k} step x {len(times)}" if r == w["rows"] else
-              f"{r}x{c}x{k} periodic patch (1/{w['rows'] // r} of the workload; updates/s is "
-              f"size-independent) x {len(times)}")
+    steps = args.steps if args.workload == "cfg3" else min(args.steps, 3)
+    times, threads = cpu_port_sample(w["cpu_rows"], w["cols"], w["levels"], args.warmup, steps=steps)
+    cpu = cpu_record(w, times, threads)
+    value = cpu["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": len(times), "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": cpu["ms_per_step"],
         "higher_is_better": True, "scaling": w["scaling"], "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": w["label"], "rows": w["rows"], "cols": c, "levels": k},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample + " (reference.transport_step restated in C, oracle/c)"},
+        "config": workload_config(w, world),
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_python_ref:
+        try:
+            line["reference_python"] = reference_python_record(w, args.python_ref_reps)
+        except Exception as e:  # the record is informational: never lose the line over it
+            line["reference_python"] = {"unavailable": f"{type(e).__name__}: {e}"}
     print(json.dumps(line), flush=True)
 
 
@@ -187,11 +247,148 @@ def run_reference(args):
 # our arm
 
 
+def _exchange_mode(requested: str, rank: int, world: int, local: int, shared: bool):
+    """p2p only when both ring neighbours (global rank +- 1) are on this host with peer
+    access from this device; otherwise every rank takes the NCCL exchange."""
+    import torch
+    import torch.distributed as dist
+
+    if world == 1 or shared:
+        return requested, None
+    info = [None] * world
+    dist.all_gather_object(info, (socket.gethostname(), local))
+    host = info[rank][0]
+    note = None
+    mode = requested
+    if requested == "p2p":
+        for nb in {(rank - 1) % world, (rank + 1) % world} - {rank}:
+            h, dev = info[nb]
+            if h != host:
+                note = f"ring neighbour rank {nb} is on host {h}: NCCL exchange"
+            elif not torch.cuda.can_device_access_peer(local, dev):
+                note = f"no peer access from cuda:{local} to cuda:{dev}: NCCL exchange"
+        flag = torch.tensor([note is not None], dtype=torch.int32, device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX)  # every rank takes the same exchange
+        if flag.item():
+            mode = "nccl"
+            note = note or "a rank cannot reach its neighbours peer to peer: NCCL exchange"
+    return mode, note
+
+
+def _timed_steps(stepper, steps, stream, flush_l2=None):
+    """Per-step device times (ms) of ``steps`` step+swap pairs on ``stream``."""
+    import torch
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for s in range(steps):
+        torch.cuda._sleep(SLEEP_CYCLES)  # keeps the launch queue ahead of the GPU
+        if flush_l2 is not None:
+            flush_l2()  # evict the previous step's data from L2 (outside the events)
+        evs[s][0].record(stream)
+        stepper.step(DT, PIVBZ)
+        evs[s][1].record(stream)
+        stepper.swap()
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def _max_over_ranks(x: float, world: int, shared: bool) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else "cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def o1280_strong(args, rank, world, shared, barrier, peak):
+    """configs[4] strong scaling: the O1280-class patch in `world` strips, same path."""
+    import torch
+
+    from paper_1908_06094_b200.distributed import StripStepper
+    from paper_1908_06094_b200.workloads import mpdata_algorithmic_bytes
+
+    w = WORKLOADS["o1280"]
+    R, C, K = w["rows"], w["cols"], w["levels"]
+    st = StripStepper(R, C, K, rank, world, seed=0, mode=args.exchange)
+    for _ in range(3):
+        st.step(DT, PIVBZ)
+        st.swap()
+    torch.cuda.synchronize()
+    if world > 1:
+        st.check()
+    barrier()
+    ms = _timed_steps(st, args.o1280_steps, torch.cuda.current_stream())
+    barrier()
+    if world > 1:
+        st.finish()
+        st.check()
+    t = _max_over_ranks(sum(ms) / 1e3, world, shared) / len(ms)
+    mine = mpdata_algorithmic_bytes(st.nrows, C, K)
+    rec = {"value": R * C * K / t, "unit": UNIT, "n_gpus": world, "scaling": "strong",
+           "ms_per_step": t * 1e3, "step_ms": step_stats(ms), "steps": len(ms),
+           "config": workload_config(w, world), "rows_per_gpu": st.nrows,
+           "effective_gbs": mine / t / 1e9, "roofline_frac": mine / t / 1e9 / peak,
+           "path": f"StripStepper ({'periodic patch' if world == 1 else st.mode + ' exchange'})",
+           "inputs": "on-device counter hash of global ids (identical for every N)",
+           "l2": "no flush: per-GPU state >= 6.3 GB",
+           "efficiency": "T1 / (N * T_N) with T1 = the N = 1 run's o1280_strong.ms_per_step"}
+    del st
+    torch.cuda.empty_cache()
+    return rec
+
+
+def e2e_time_loop(w: dict, steps: int) -> dict:
+    """The reference's dependent time loop through the drop-in API on host Fields."""
+    from paper_1908_06094_b200 import (MpdataParams, PatchSpec, TileSpec, build_geometry, build_mpdata,
+                                       build_state, flat_to_field, halo_update, run_fused)
+    from paper_1908_06094_b200.workloads import transport_inputs
+
+    R, C, K = w["rows"], w["cols"], w["levels"]
+    spec = PatchSpec(R, C, K)
+    inp = transport_inputs(R, C, K, 0, "uniform", "gaussian-bump", "one", signs=False)
+    state = build_state(spec)
+    geo = build_geometry(spec, "uniform", seed=0)
+    for name in ("pd_in", "vn", "wn", "rho"):
+        f = getattr(state, name)
+        flat_to_field(inp[{"pd_in": "pd"}.get(name, name)], f)
+        halo_update(f)
+    comp = build_mpdata(spec, state, geo, MpdataParams(DT, PIVBZ))
+    tiles = TileSpec(R, C, 1)
+    h = spec.halo
+
+    def copy_core(src, dst):  # the reference's bench._copy_core (bench.py:430-435)
+        values = src.array("primary", "r")[h:h + R, :, h:h + C, :, :]
+        dst.array("primary", "rw")[h:h + R, :, h:h + C, :, :] = values
+        halo_update(dst)
+
+    times = []
+    for step in range(steps + 2):  # two untimed warm-up steps
+        t0 = time.perf_counter()
+        if step:
+            copy_core(state.pd_out, state.pd_in)
+        run_fused(comp, tiles)
+        times.append(time.perf_counter() - t0)
+    times = times[2:]
+    t = statistics.median(times)
+    nb = state.pd_in.linear.total * 8
+    return {"value": R * C * K / t, "unit": UNIT, "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb,
+            "ms_per_step": t * 1e3, "step_ms": step_stats([x * 1e3 for x in times]),
+            "api": f"reference loop (bench.py:398-403): _copy_core(pd_out, pd_in) on the host Fields, "
+                   f"then run_fused(comp, TileSpec({R}, {C}, 1)); per step the pd_in host buffer "
+                   "(page-locked LinearLayout) H2D + device reorder, fused step, reorder + pd_out D2H "
+                   "into its host buffer, host core copy + halo refresh; dependent steps, no overlap"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_1908_06094_b200 import PatchSpec, StructuredStepper, _lib
+    from paper_1908_06094_b200.distributed import StripStepper
     from paper_1908_06094_b200.workloads import (mpdata_2d_bytes, mpdata_algorithmic_bytes,
                                                  paper_model_bytes, transport_inputs)
 
@@ -213,191 +410,168 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
+    args.exchange, exchange_note = _exchange_mode(args.exchange, rank, world, local, shared)
     w = WORKLOADS[args.workload]
     K, cols = w["levels"], w["cols"]
-    global_rows = w["rows"] * world if w["scaling"] == "weak" else w["rows"]
+    cfg = workload_config(w, world)
+    global_rows = cfg["rows"]
     GV = global_rows * cols  # vertices of the whole job
-    host_fed = args.workload == "cfg3" and world == 1
-    exchange_note = None
-    if world > 1 and not shared and args.exchange == "p2p":
-        # the fused exchange stores into the neighbours' memory: it needs peer access
-        # (NVLink / NVSwitch); without it the NCCL send/recv exchange runs instead
-        nbrs = {(local + 1) % world, (local - 1) % world} - {local}
-        if not all(torch.cuda.can_device_access_peer(local, d) for d in nbrs):
-            exchange_note = f"no peer access from cuda:{local} to {sorted(nbrs)}: NCCL exchange"
-            args.exchange = "nccl"
-        flag = torch.tensor([args.exchange == "nccl"], dtype=torch.int32, device="cuda")
-        dist.all_reduce(flag, op=dist.ReduceOp.MAX)  # every rank takes the same exchange
-        if flag.item():
-            args.exchange = "nccl"
-            exchange_note = exchange_note or "a rank lacks peer access to its neighbours: NCCL exchange"
-    if not host_fed:
-        from paper_1908_06094_b200.distributed import StripStepper
-
+    peak, peak_src = _peaks()
+    stream = torch.cuda.current_stream()
+    with ClockSampler(0 if shared else local) as clocks:
+        # every rank steps its strip through the same path at every N; the cfg3 strips carry
+        # the reference's _transport_setup fields of one 279x256x80 patch each
         stepper = StripStepper(global_rows, cols, K, rank, world, seed=0, mode=args.exchange)
         my_rows = stepper.nrows
-    else:
-        my_rows = ROWS
-        inp = transport_inputs(ROWS, COLS, K, 0, "uniform", "gaussian-bump", "one")
-        stepper = StructuredStepper(PatchSpec(ROWS, COLS, K))
-        stepper.set_geometry(inp["signs"], inp["dual"])
-        stepper.upload(inp["pd"], inp["vn"], inp["wn"], inp["rho"])
-    stream = torch.cuda.current_stream()
-    # L2 flush by READING 256 MiB (> 126 MB L2): leaves only clean lines behind, so the
-    # timed step pays no write-back of someone else's dirty data
-    flush = torch.ones(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
-    flush_sink = torch.empty(1, dtype=torch.float64, device="cuda")
+        inp = None
+        if args.workload == "cfg3":
+            inp = transport_inputs(w["rows"], cols, K, 0, "uniform", "gaussian-bump", "one", signs=False)
+            stepper.load_flat(inp["pd"], inp["vn"], inp["wn"], inp["rho"], inp["dual"].reshape(-1, 1))
+        # L2 flush by READING 256 MiB (> 126 MB L2): leaves only clean lines behind, so the
+        # timed step pays no write-back of someone else's dirty data
+        flush = torch.ones(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+        flush_sink = torch.empty(1, dtype=torch.float64, device="cuda")
 
-    def flush_l2():
-        flush_sink.copy_(flush.sum().reshape(1))
+        def flush_l2():
+            flush_sink.copy_(flush.sum().reshape(1))
 
-    for _ in range(args.warmup):
-        stepper.step(DT, PIVBZ)
-        stepper.swap()
-    torch.cuda.synchronize()
-    if not host_fed:
-        stepper.check()  # a broken exchange fails here, not after every timed step has timed out
-    barrier()
-
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    with ClockSampler(local) as clocks:
+        for _ in range(args.warmup):
+            stepper.step(DT, PIVBZ)
+            stepper.swap()
+        torch.cuda.synchronize()
+        if world > 1:
+            stepper.check()  # a broken exchange fails here, not after every timed step has timed out
         barrier()
         torch.cuda.synchronize()
         t_wall0 = time.perf_counter()
-        for s in range(args.steps):
-            flush_l2()  # evict the previous step's data from L2 (outside the events)
-            evs[s][0].record(stream)
-            stepper.step(DT, PIVBZ)
-            evs[s][1].record(stream)
-            stepper.swap()
-        torch.cuda.synchronize()
+        step_ms = _timed_steps(stepper, args.steps, stream, flush_l2)
         barrier()
         t_wall = time.perf_counter() - t_wall0
-    if not host_fed:
-        stepper.finish()
-        stepper.check()
-    step_ms = [a.elapsed_time(b) for a, b in evs]
-    total_s = sum(step_ms) / 1e3
-    if world > 1:
-        t = torch.tensor([total_s], dtype=torch.float64, device="cpu" if shared else "cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_s = float(t.item())
-    mean_step = total_s / args.steps
-    value = GV * K / mean_step
-    V = my_rows * cols
+        if world > 1:
+            stepper.finish()
+            stepper.check()
+        total_s = _max_over_ranks(sum(step_ms) / 1e3, world, shared)
+        mean_step = total_s / args.steps
+        value = GV * K / mean_step
+        variant = _lib.lib().tsg_fused_variant_of(stepper.grid.handle, 0, my_rows)
+        band = world == 1 and _lib.lib().tsg_fused_band_of(stepper.grid.handle, 0, my_rows) == 1
+        hits = _lib.ctypes.c_int64()
+        misses = _lib.ctypes.c_int64()
+        _lib.call("tsg_launch_cache_stats", stepper.grid.handle, _lib.ctypes.byref(hits),
+                  _lib.ctypes.byref(misses))
+        del stepper
+        torch.cuda.empty_cache()
 
-    # e2e through the public flat API from pinned host buffers (N=1): every step copies its
-    # inputs H2D, reorders them into the structured layout, steps, reorders back and copies
-    # pd_out D2H; StructuredStepper.run_pipelined overlaps step n+1's H2D with step n's GPU
-    # work and step n-1's D2H (PCIe is full duplex).  Primary: the reference's time loop
-    # (only the density state crosses PCIe, vn / wn / rho stay resident); secondary: the
-    # flat oracle call pattern (every input every step).
-    e2e = e2e_all = None
-    if host_fed:
-        pinned = [torch.from_numpy(np.ascontiguousarray(inp[n])).pin_memory()
-                  for n in ("pd", "vn", "wn", "rho")]
-        outs = [torch.empty((V, K), dtype=torch.float64).pin_memory() for _ in range(2)]
-        d2h = outs[0].numel() * 8
-        e2e_steps = max(4, min(args.steps, 40))
+        host_fed = args.workload == "cfg3" and world == 1
+        e2e = e2e_all = loop = e2e_loop = None
+        if host_fed:
+            V = my_rows * cols
+            st = StructuredStepper(PatchSpec(w["rows"], cols, K))
+            sig = transport_inputs(w["rows"], cols, K, 0, "uniform", "gaussian-bump", "one")["signs"]
+            st.set_geometry(sig, inp["dual"])
+            st.upload(inp["pd"], inp["vn"], inp["wn"], inp["rho"])
+            pinned = [torch.from_numpy(np.ascontiguousarray(inp[n])).pin_memory()
+                      for n in ("pd", "vn", "wn", "rho")]
+            outs = [torch.empty((V, K), dtype=torch.float64).pin_memory() for _ in range(2)]
+            d2h = outs[0].numel() * 8
+            e2e_steps = max(4, min(args.steps, 40))
 
-        def e2e_run(step_inputs, api):
-            stepper.run_pipelined([pinned] * 3, outs + outs[:1], DT, PIVBZ)  # warm-up (all inputs)
+            def e2e_run(step_inputs, api):
+                st.run_pipelined([pinned] * 3, outs + outs[:1], DT, PIVBZ)  # warm-up (all inputs)
+                torch.cuda.synchronize()
+                e0, e1 = st.run_pipelined([step_inputs] * e2e_steps,
+                                          [outs[n % 2] for n in range(e2e_steps)], DT, PIVBZ)
+                torch.cuda.synchronize()
+                t_e2e = e0.elapsed_time(e1) / 1e3 / e2e_steps
+                h2d = sum(t.numel() * 8 for t in step_inputs if t is not None)
+                return {"value": V * K / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3,
+                        "pcie_gbs": (h2d + d2h) / t_e2e / 1e9, "api": api}
+
+            e2e = e2e_run([pinned[0], None, None, None],
+                          "independent host-fed steps: StructuredStepper.run_pipelined, each step "
+                          "H2D of a density state pd (flat canonical, pinned), on-GPU reorder, fused "
+                          "step, reorder, D2H of pd_out; vn / wn / rho resident (fixed, as in the "
+                          "reference's loop); steps overlapped (H2D n+1 | GPU n | D2H n-1) since they "
+                          "do not depend on each other -- see e2e_time_loop for the dependent loop")
+            e2e_all = e2e_run(pinned, "independent host-fed steps as e2e, with every input (pd / vn / "
+                                      "wn / rho, the flat oracle call of reference.py:93-116) copied "
+                                      "H2D per step")
+            # back-to-back device time loop (tsg_mpdata_run ping-pong, no flush: 320 MB > L2)
+            n_loop = 100
+            st.run(n_loop, DT, PIVBZ)
             torch.cuda.synchronize()
-            e0, e1 = stepper.run_pipelined([step_inputs] * e2e_steps,
-                                           [outs[n % 2] for n in range(e2e_steps)], DT, PIVBZ)
+            l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            l0.record(stream)
+            st.run(n_loop, DT, PIVBZ)
+            l1.record(stream)
             torch.cuda.synchronize()
-            t_e2e = e0.elapsed_time(e1) / 1e3 / e2e_steps
-            h2d = sum(t.numel() * 8 for t in step_inputs if t is not None)
-            return {"value": V * K / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3,
-                    "pcie_gbs": (h2d + d2h) / t_e2e / 1e9, "api": api}
-
-        e2e = e2e_run([pinned[0], None, None, None],
-                      "StructuredStepper.run_pipelined, the reference's time loop (bench.py:398-403): "
-                      "per step H2D of the density state pd (flat canonical, pinned), on-GPU reorder, "
-                      "fused step, reorder, D2H of pd_out; vn / wn / rho fixed and resident")
-        e2e_all = e2e_run(pinned, "StructuredStepper.run_pipelined, the flat oracle call pattern "
-                                  "(reference.py:93-116): H2D of pd / vn / wn / rho every step")
-
-    # back-to-back time loop (tsg_mpdata_run ping-pong, no L2 flush: the 320 MB of inputs
-    # exceed the 126 MB L2), the reference's bench loop (bench.py:398-403) -- informational
-    loop = None
-    if host_fed:
-        n_loop = 100
-        stepper.run(n_loop, DT, PIVBZ)
-        torch.cuda.synchronize()
-        l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        l0.record(stream)
-        stepper.run(n_loop, DT, PIVBZ)
-        l1.record(stream)
-        torch.cuda.synchronize()
-        t_loop = l0.elapsed_time(l1) / 1e3 / n_loop
-        loop = {"value": V * K / t_loop, "unit": UNIT, "ms_per_step": t_loop * 1e3, "steps": n_loop,
-                "l2": "no flush: inputs (320 MB) larger than L2",
-                "api": "StructuredStepper.run (tsg_mpdata_run, one fused launch per step)"}
+            t_loop = l0.elapsed_time(l1) / 1e3 / n_loop
+            loop = {"value": V * K / t_loop, "unit": UNIT, "ms_per_step": t_loop * 1e3, "steps": n_loop,
+                    "l2": "no flush: inputs (320 MB) larger than L2",
+                    "api": "StructuredStepper.run (tsg_mpdata_run, captured two-step graph)"}
+            del st
+            torch.cuda.empty_cache()
+            e2e_loop = e2e_time_loop(w, max(5, min(args.steps, 20)))
+        o1280 = None
+        if args.workload == "cfg3" and not args.no_o1280:
+            o1280 = o1280_strong(args, rank, world, shared, barrier, peak)
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
 
-    peak, peak_src = _peaks()
     bcomp = mpdata_algorithmic_bytes(my_rows, cols, K)
     achieved = bcomp / mean_step / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     tfile = ROOT / "profiles" / "fused_traffic.json"
-    if tfile.exists() and host_fed:  # the ncu capture is of the 279x256x80 launch
-        traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
-    from paper_1908_06094_b200._lib import lib as _l
+    if tfile.exists() and world == 1 and args.workload == "cfg3":
+        tj = json.loads(tfile.read_text())  # the ncu capture of the 279x256x80 launch
+        traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("source")
     import ctypes
 
     vi = [ctypes.c_int() for _ in range(6)]
-    variant = _l().tsg_fused_variant_of(stepper.grid.handle, 0, my_rows)
-    band = world == 1 and _l().tsg_fused_band_of(stepper.grid.handle, 0, my_rows) == 1
-    _l().tsg_fused_variant_info(variant, *[ctypes.byref(x) for x in vi])
+    _lib.lib().tsg_fused_variant_info(variant, *[ctypes.byref(x) for x in vi])
     cpu = None
     if not args.no_cpu and world == 1:  # the host baseline is measured at N = 1 only
-        cr = w["cpu_rows"]
-        times, threads = cpu_reference_steps(0, 1 if cr == w["rows"] else 0, budget_s=args.cpu_seconds,
-                                             rows=cr, cols=cols, levels=K)
-        tc = statistics.median(times)
-        cpu = {"value": cr * cols * K / tc, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": (f"{cr}x{cols}x{K} periodic patch" + ("" if cr == w["rows"] else
-                          f" (1/{w['rows'] // cr} of the per-job patch; updates/s is size-independent)"))
-                         + f", step x {len(times)} (median), reference.transport_step restated in C "
-                           "(oracle/c), OpenMP"}
+        times, threads = cpu_port_sample(w["cpu_rows"], cols, K, args.warmup, budget_s=args.cpu_seconds)
+        cpu = cpu_record(w, times, threads)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": mean_step * 1e3, "higher_is_better": True,
         "scaling": w["scaling"], "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic" + ("" if host_fed else " (on-device counter-hash fields)"),
-        "config": {"workload": w["label"], "rows": global_rows, "cols": cols, "levels": K,
-                   "rows_per_gpu": my_rows, "vertices": GV, "edges": 3 * GV,
-                   "dt": DT, "pivbz": PIVBZ, "parallelism": f"row-strips x{world}",
-                   "halo_exchange": ("none" if world == 1 else
-                                     "one launch per step: boundary-row epilogue stores into the "
-                                     "neighbours' halos (CUDA IPC over NVLink), in-kernel step fence"
-                                     if args.exchange == "p2p" else "NCCL grouped send/recv"),
-                   **({"exchange_fallback": exchange_note} if exchange_note else {}),
-                   "l2": "256 MiB read-only L2 flush before every timed step (outside the events)",
-                   "fused_schedule": ("band round robin" if band else "contiguous ranges"),
-                   "fused_tile": {"variant": variant, "ti": vi[0].value, "tj": vi[1].value, "kc": vi[2].value,
-                                  "stages": vi[3].value, "threads": vi[4].value,
-                                  "smem_bytes": vi[5].value}},
-        "ms_per_step_median": statistics.median(step_ms) if step_ms else None,
+        "data": "synthetic (" + ("the reference's _transport_setup fields of a 279x256x80 patch per strip"
+                                 if args.workload == "cfg3" else "on-device counter-hash fields") + ")",
+        "config": cfg,
+        "setup": {"rows_per_gpu": my_rows, "vertices": GV, "edges": 3 * GV, "dt": DT, "pivbz": PIVBZ,
+                  "path": "StripStepper" + (" (periodic patch)" if world == 1 else f" ({args.exchange})"),
+                  "parallelism": f"row-strips x{world}",
+                  "halo_exchange": ("none" if world == 1 else
+                                    "one launch per step: boundary-row epilogue stores into the "
+                                    "neighbours' halos (CUDA IPC over NVLink), in-kernel step fence"
+                                    if args.exchange == "p2p" else "NCCL grouped send/recv"),
+                  **({"exchange_fallback": exchange_note} if exchange_note else {}),
+                  "l2": "256 MiB read-only L2 flush before every timed step (outside the events)",
+                  "fused_schedule": ("band round robin" if band else "contiguous ranges"),
+                  "fused_tile": {"variant": variant, "ti": vi[0].value, "tj": vi[1].value, "kc": vi[2].value,
+                                 "stages": vi[3].value, "threads": vi[4].value, "smem_bytes": vi[5].value},
+                  "launch_cache": {"hits": hits.value, "misses": misses.value}},
+        "step_ms": step_stats(step_ms),
         "effective_gbs": achieved,
         "paper_model_gbs": paper_model_bytes(my_rows, cols, K) / mean_step / 1e9,
         "stage_updates_per_s": GV * (6 * K + 1) / mean_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bcomp,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_source": peak_src, "algorithmic_bytes_per_launch": bcomp,
                      "bytes_2d_per_launch": mpdata_2d_bytes(my_rows, cols),
                      "per": "rank 0's fused launch(es) per step"},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "e2e_all_inputs": e2e_all,
+        "e2e_time_loop": e2e_loop,
         "time_loop": loop,
+        "o1280_strong": o1280,
         "gpu_launches": args.steps * (1 if world == 1 or args.exchange == "p2p" else 3),
         "clocks": clocks.summary(),
         "timed_wall_s": t_wall,
@@ -420,8 +594,14 @@ def main(argv=None):
                     help="N>1 halo exchange: fused P2P epilogue stores (default) or NCCL send/recv")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3",
                     help="cfg3 (headline, weak scaling) or o1280 (strong scaling)")
+    ap.add_argument("--o1280-steps", type=int, default=20,
+                    help="timed steps of the o1280_strong record (cfg3 runs)")
+    ap.add_argument("--no-o1280", action="store_true", help="skip the o1280_strong record")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-python-ref", action="store_true",
+                    help="reference arm: skip timing the reference package itself")
+    ap.add_argument("--python-ref-reps", type=int, default=3)
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

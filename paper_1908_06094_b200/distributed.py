@@ -132,12 +132,72 @@ def wait_all(reqs) -> None:
         r.wait()
 
 
+class LocalRing:
+    """In-process stand-in for the NCCL halo exchange between the StripSteppers of one
+    process (one GPU), with the semantics of :func:`exchange_halo_rows` under NCCL: a
+    rank's call sends its first / last interior row into the up / down neighbour's halo
+    row of the same field (matched by attribute name) with device copies on the calling
+    stream, and returns requests whose ``wait()`` makes the then-current stream wait for
+    that rank's sends AND receives -- the copies a neighbour issues into it later in the
+    same exchange round are appended to the list it already holds (StripStepper keeps the
+    list as ``pending`` until its next step).  Ranks step in order and swap after all of
+    them stepped.  Used by the GPU tests of ``mode="nccl"`` (pending / comm-stream / event
+    ordering of StripStepper.step)."""
+
+    class _Req:
+        def __init__(self, event):
+            self.event = event
+
+        def wait(self):
+            torch.cuda.current_stream().wait_event(self.event)
+
+    _NAMES = ("pd", "pd_out", "vn", "wn", "rho", "dual", "signs")
+
+    def __init__(self):
+        self.steppers = {}
+        self.calls = {}    # (rank, name) -> exchange rounds made
+        self.current = {}  # (rank, name) -> request list returned in the latest round
+        self.queued = {}   # (rank, name) -> requests of receives that precede its own call
+
+    def add(self, stepper: "StripStepper") -> None:
+        self.steppers[stepper.rank] = stepper
+
+    def __call__(self, field, nrows, rank, world, group=None):
+        if world == 1 or len(self.steppers) < world:
+            return []  # construction time: exchanged once every rank exists (static())
+        me = self.steppers[rank]
+        name = next(n for n in self._NAMES if getattr(me, n) is field)
+        round_ = self.calls.get((rank, name), 0) + 1
+        self.calls[(rank, name)] = round_
+        ups, downs = (rank - 1) % world, (rank + 1) % world
+        up, down = getattr(self.steppers[ups], name), getattr(self.steppers[downs], name)
+        up[up.shape[0] - 1].copy_(field[1], non_blocking=True)  # first interior -> up's bottom halo
+        down[0].copy_(field[nrows], non_blocking=True)          # last interior -> down's top halo
+        done = torch.cuda.Event()
+        done.record(torch.cuda.current_stream())
+        mine = [self._Req(done)] + self.queued.pop((rank, name), [])
+        self.current[(rank, name)] = mine
+        for nb in {ups, downs}:
+            if self.calls.get((nb, name), 0) >= round_:  # it already holds this round's list
+                self.current[(nb, name)].append(self._Req(done))
+            else:
+                self.queued.setdefault((nb, name), []).append(self._Req(done))
+        return mine
+
+    def static(self) -> None:
+        """The setup exchange of the static inputs, once every rank's stepper exists."""
+        for st in self.steppers.values():
+            st._exchange_static()
+        torch.cuda.synchronize()
+
+
 class StripStepper:
     """One rank's strip of a (global_rows x cols x K) patch, stepped on the device.
 
     Inputs are synthetic (on-device counter hash of global ids, identical for every
-    decomposition) unless loaded with :meth:`load_flat`.  ``world == 1`` degenerates to
-    the periodic single-patch step.
+    decomposition) unless loaded with :meth:`load_flat` (flat canonical arrays of this
+    strip's rows, e.g. the reference's ``_transport_setup`` fields).  ``world == 1``
+    degenerates to the periodic single-patch step.
     """
 
     def __init__(self, global_rows: int, cols: int, levels: int, rank: int, world: int,
@@ -224,6 +284,32 @@ class StripStepper:
         self.signs[:, 0, 1:-1, :] = strip
         self.signs[:, 0, 0, :] = strip[:, -1, :]
         self.signs[:, 0, -1, :] = strip[:, 0, :]
+        self._exchange_static()
+
+    def load_flat(self, pd, vn, wn, rho, dual=None) -> None:
+        """Replace the inputs by flat ``[element, level]`` arrays of this strip's rows in
+        canonical order (vertex (i, j) -> row (i - row0) * cols + j, edge (i, c, j) ->
+        ((i - row0) * 3 + c) * cols + j); numpy or CUDA.  ``dual`` (one value per vertex)
+        defaults to the current one.  Halo rows are then exchanged once, as at setup.
+        Every rank must call it (the exchange is collective)."""
+        import numpy as np
+
+        nv = self.nrows * self.cols
+        want = {"pd": (nv, self.K), "vn": (3 * nv, self.K), "wn": (nv, self.K + 1), "rho": (nv, self.K)}
+        src = {"pd": pd, "vn": vn, "wn": wn, "rho": rho}
+        if dual is not None:
+            want["dual"], src["dual"] = (nv, 1), dual
+        s = _lib.stream_handle()
+        for name, shape in want.items():
+            x = src[name]
+            t = (x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x)))
+            t = t.to(device=self.grid.device, dtype=torch.float64).reshape(-1).contiguous()
+            if t.numel() != shape[0] * shape[1]:
+                raise ValueError(f"{name} must hold {shape[0]} x {shape[1]} values for this strip, "
+                                 f"got {t.numel()}")
+            loc = 2 if name == "vn" else 0
+            _lib.call("tsg_pack", self.grid.handle, loc, shape[1], _lib.ptr(t), None,
+                      _lib.ptr(getattr(self, name)), s)
         self._exchange_static()
 
     def _exchange_static(self) -> None:

@@ -131,6 +131,81 @@ def test_strip_steppers_on_one_gpu_match_single_patch(cuda_ok):
     assert torch.equal(got, single.interior("pd"))
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,shape", [(2, (16, 29, 18)), (3, (23, 37, 21)), (4, (64, 40, 33))])
+def test_nccl_mode_step_with_in_process_exchanger(cuda_ok, world, shape):
+    """StripStepper.step() in mode="nccl" end to end: interior rows overlapped with the
+    previous exchange, wait on the pending requests, boundary rows, then the exchange of
+    pd_out issued on the comm stream after a recorded event -- with LocalRing standing in
+    for batch_isend_irecv (device copies on the comm stream, waitable requests covering
+    sends and receives).  Bitwise equal to the single-patch step after 5 steps."""
+    from paper_1908_06094_b200.distributed import LocalRing, StripStepper
+
+    rows, cols, K = shape
+    ring = LocalRing()
+    steppers = [StripStepper(rows, cols, K, r, world, seed=11, exchange=ring, mode="nccl")
+                for r in range(world)]
+    for st in steppers:
+        ring.add(st)
+    ring.static()
+    single = StripStepper(rows, cols, K, 0, 1, seed=11)
+    for _ in range(5):
+        single.step(0.2, 0.8)
+        single.swap()
+        for st in steppers:
+            st.step(0.2, 0.8)
+        for st in steppers:
+            st.swap()
+    for st in steppers:
+        st.finish()
+    torch.cuda.synchronize()
+    assert all(st.comm is not torch.cuda.current_stream() for st in steppers)
+    got = torch.cat([st.interior("pd") for st in steppers], 0)
+    assert torch.equal(got, single.interior("pd"))
+    # the pd_out halo rows received by the last exchange hold the neighbours' rows
+    for r, st in enumerate(steppers):
+        up, down = steppers[(r - 1) % world], steppers[(r + 1) % world]
+        assert torch.equal(st.pd[0], up.pd[up.nrows]) and torch.equal(st.pd[st.nrows + 1], down.pd[1])
+
+
+@pytest.mark.gpu
+def test_strip_load_flat_matches_the_oracle(cuda_ok):
+    """load_flat: the reference's flat inputs (row slices per strip) -> strips; one patch
+    (world 1) and 3 in-process strips both equal the oracle's step bitwise."""
+    from oracle import tsg_oracle as O
+    from paper_1908_06094_b200.distributed import LocalRing, StripStepper
+
+    rows, cols, K, dt, pivbz = 21, 26, 12, 0.2, 0.8
+    inp = O.transport_inputs(rows, cols, K, 4, "uniform", "random", "random")
+    want = O.step_inputs(rows, cols, inp, dt, pivbz)["pd_out"].reshape(rows, cols, K)
+
+    def rows_of(name, r0, n):
+        a = inp[name]
+        per = a.shape[0] // rows
+        return a[r0 * per:(r0 + n) * per]
+
+    single = StripStepper(rows, cols, K, 0, 1)
+    single.load_flat(inp["pd"], inp["vn"], inp["wn"], inp["rho"], inp["dual"].reshape(-1, 1))
+    single.step(dt, pivbz)
+    torch.cuda.synchronize()
+    assert np.array_equal(single.interior("pd_out")[:, 0, :, :K].cpu().numpy(), want)
+    ring = LocalRing()
+    steppers = [StripStepper(rows, cols, K, r, 3, exchange=ring) for r in range(3)]
+    for st in steppers:
+        ring.add(st)
+    for st in steppers:
+        st.load_flat(*(rows_of(n, st.row0, st.nrows) for n in ("pd", "vn", "wn", "rho")),
+                     rows_of("dual", st.row0, st.nrows).reshape(-1, 1))
+    torch.cuda.synchronize()
+    for st in steppers:
+        st.step(dt, pivbz)
+    torch.cuda.synchronize()
+    got = torch.cat([st.interior("pd_out") for st in steppers], 0)[:, 0, :, :K].cpu().numpy()
+    assert np.array_equal(got, want)
+    with pytest.raises(ValueError, match="values for this strip"):
+        single.load_flat(inp["pd"][:-1], inp["vn"], inp["wn"], inp["rho"])
+
+
 def _p2p_worker(rank, world, port, q, single_launch=True, graph=False, shape=(17, 29, 18)):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
