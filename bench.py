@@ -435,10 +435,7 @@ def run_ours(args):
         def flush_l2():
             flush_sink.copy_(flush.sum().reshape(1))
 
-        for _ in range(args.warmup):
-            stepper.step(DT, PIVBZ)
-            stepper.swap()
-        torch.cuda.synchronize()
+        _timed_steps(stepper, args.warmup, stream, flush_l2)  # warm-up = the timed sequence
         if world > 1:
             stepper.check()  # a broken exchange fails here, not after every timed step has timed out
         barrier()
@@ -558,6 +555,7 @@ def run_ours(args):
                                  "stages": vi[3].value, "threads": vi[4].value, "smem_bytes": vi[5].value},
                   "launch_cache": {"hits": hits.value, "misses": misses.value}},
         "step_ms": step_stats(step_ms),
+        **({"step_ms_all": [round(x, 5) for x in step_ms]} if len(step_ms) <= 64 else {}),
         "effective_gbs": achieved,
         "paper_model_gbs": paper_model_bytes(my_rows, cols, K) / mean_step / 1e9,
         "stage_updates_per_s": GV * (6 * K + 1) / mean_step,

@@ -161,6 +161,10 @@ int tsg_time_loop_graphs_built(void);
  * fused step, keyed by all of its arguments): hits / misses so far.  A diagnostic; a
  * repeated step with the same buffers encodes nothing. */
 int tsg_launch_cache_stats(const tsg_grid *g, int64_t *hits, int64_t *misses);
+/* Debug trace of the fused kernel (no reference counterpart; a measurement aid): fused
+ * launches prepared while set write, per CTA b, per_cta4[4b .. 4b+3] = {globaltimer ns at
+ * entry, when its first stage landed, when its unit loop ended, units run}.  NULL = off. */
+int tsg_debug_trace(uint64_t *per_cta4);
 int tsg_mpdata_run_strip(tsg_grid *g, double *pd_a, double *pd_b, const double *vn,
                          const double *wn, const double *rho, const double *signs,
                          const double *dual, double dt, double pivbz, int flux_op,

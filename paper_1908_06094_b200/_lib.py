@@ -60,6 +60,7 @@ SIGNATURES = {
     "tsg_set_fused_band": (_c_int, [_c_int]),
     "tsg_time_loop_graphs_built": (_c_int, []),
     "tsg_launch_cache_stats": (_c_int, [_p, ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i64)]),
+    "tsg_debug_trace": (_c_int, [_p]),
     "tsg_fused_variant_info": (_c_int, [_c_int] + [ctypes.POINTER(_c_int)] * 6),
     "tsg_neighbor_reduce": (_c_int, [_p, _c_int, _c_int, _c_int, _p, _p, _p, _p]),
     "tsg_neighbor_reduce_indirect": (_c_int, [_p, _c_i64, _c_int, _c_int, _p, _p, _p, _p]),

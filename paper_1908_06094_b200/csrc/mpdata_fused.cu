@@ -74,6 +74,14 @@ struct FusedCfg {
 constexpr int kProbeOp = 99;
 // flux_op value of the compute probe (arithmetic on unloaded shared memory, no TMA)
 constexpr int kComputeProbe = 98;
+// flux_op values of the load probes (attribution of DRAM traffic and time per field): the
+// TMA pipeline with only pd (90), vn (91), wn (92) or rho (93) loaded, or all four (94),
+// and no arithmetic and no stores
+constexpr int kLoadProbe = 90, kLoadProbeAll = 94;
+template <int OP> __host__ __device__ constexpr bool is_load_probe() { return OP >= kLoadProbe && OP <= kLoadProbeAll; }
+template <int OP> __host__ __device__ constexpr bool loads_field(int f) {
+    return !is_load_probe<OP>() || OP == kLoadProbeAll || OP == kLoadProbe + f;
+}
 
 struct FusedArgs {
     const double *signs;  // vertex field, inner 6
@@ -100,6 +108,9 @@ struct FusedArgs {
     double dt, pivbz;
     int tiles_i, tiles_j, chunks;
     int64_t units;
+    // debug trace (tsg_debug_trace): per CTA {entry, first stage landed, loop end, units}
+    // in globaltimer ns, or NULL
+    uint64_t *trace;
 };
 
 // BAND schedule (large patches, single-GPU launches): whole tiles dealt round robin in
@@ -208,6 +219,7 @@ __global__ void __launch_bounds__(TI *TJ * LV + (WS ? 32 : 0), 1)
     const int n_units = BAND ? (int)((a.tiles_i * a.tiles_j - blockIdx.x + gridDim.x - 1) / gridDim.x) * a.chunks
                              : (int)(a.units * (blockIdx.x + 1) / gridDim.x) - u_begin;
 
+    if (a.trace && tid == 0) a.trace[4 * blockIdx.x] = globaltimer_ns();
     if (tid == 0) {
         prefetch_tmap(&tm_pd);
         prefetch_tmap(&tm_vn);
@@ -252,12 +264,14 @@ __global__ void __launch_bounds__(TI *TJ * LV + (WS ? 32 : 0), 1)
         const int i0 = a.row_lo + tr * TI, j0 = p_tj * TJ, k0 = p_chunk * KC;
         unsigned char *base = smem + stage * C::kStageBytes;
         uint64_t *bar = &bars[stage];
-        mbar_expect_tx(bar, C::kTxBytes);
+        constexpr uint32_t tx = (loads_field<OP>(0) ? C::kPdBytes : 0) + (loads_field<OP>(1) ? C::kVnBytes : 0) +
+                                (loads_field<OP>(2) ? C::kWnBytes : 0) + (loads_field<OP>(3) ? C::kRhoBytes : 0);
+        mbar_expect_tx(bar, tx);
         // storage coordinates: logical (i, j) -> (i + 1, j + 1)
-        tma_load_3d(base + C::kPdOff, &tm_pd, bar, k0 - 2, j0, i0);
-        tma_load_4d(base + C::kVnOff, &tm_vn, bar, k0, j0, 0, i0);
-        tma_load_3d(base + C::kWnOff, &tm_wn, bar, k0, j0 + 1, i0 + 1);
-        tma_load_3d(base + C::kRhoOff, &tm_rho, bar, k0, j0 + 1, i0 + 1);
+        if constexpr (loads_field<OP>(0)) tma_load_3d(base + C::kPdOff, &tm_pd, bar, k0 - 2, j0, i0);
+        if constexpr (loads_field<OP>(1)) tma_load_4d(base + C::kVnOff, &tm_vn, bar, k0, j0, 0, i0);
+        if constexpr (loads_field<OP>(2)) tma_load_3d(base + C::kWnOff, &tm_wn, bar, k0, j0 + 1, i0 + 1);
+        if constexpr (loads_field<OP>(3)) tma_load_3d(base + C::kRhoOff, &tm_rho, bar, k0, j0 + 1, i0 + 1);
         if (++p_chunk == a.chunks) {
             p_chunk = 0;
             if constexpr (BAND) {
@@ -337,6 +351,7 @@ __global__ void __launch_bounds__(TI *TJ * LV + (WS ? 32 : 0), 1)
         }
 
         if (OP != kComputeProbe) mbar_wait(&bars[stage], (uint32_t)((n / STAGES) & 1));
+        if (a.trace && n == 0 && tid == 0) a.trace[4 * blockIdx.x + 1] = globaltimer_ns();
 
         const double *sp = reinterpret_cast<const double *>(smem + stage * C::kStageBytes + C::kPdOff) + oP;
         const double *sv = reinterpret_cast<const double *>(smem + stage * C::kStageBytes + C::kVnOff) + oV;
@@ -346,7 +361,7 @@ __global__ void __launch_bounds__(TI *TJ * LV + (WS ? 32 : 0), 1)
 
         if constexpr (LP == 2) {
             const int k = k0 + kq;  // this thread's level pair (k, k+1)
-            if (vvalid && k < a.K) {
+            if (!is_load_probe<OP>() && vvalid && k < a.K) {
                 const double *P = sp;
                 const double *V = sv;
                 const double2 c = ld2(P);
@@ -420,7 +435,7 @@ __global__ void __launch_bounds__(TI *TJ * LV + (WS ? 32 : 0), 1)
         for (int h = 0; h < C::kLevelsPerThread; ++h) {
             const int kk = LV * h;  // level offset of this pass inside the chunk
             const int k = k0 + kl + kk;
-            if (vvalid && k < a.K && (KC % LV == 0 || kl + kk < KC)) {
+            if (!is_load_probe<OP>() && vvalid && k < a.K && (KC % LV == 0 || kl + kk < KC)) {
                 const double *P = sp + kk;
                 const double *V = sv + kk;
                 const double p0 = P[0];
@@ -489,6 +504,10 @@ __global__ void __launch_bounds__(TI *TJ * LV + (WS ? 32 : 0), 1)
             __syncthreads();  // every thread is done with this stage
         }
     }
+    if (a.trace && tid == 0) {
+        a.trace[4 * blockIdx.x + 2] = globaltimer_ns();
+        a.trace[4 * blockIdx.x + 3] = (uint64_t)n_units;
+    }
     if constexpr (WS && PEER)  // every consumer's stores are issued (consumer warps only)
         asm volatile("bar.sync 1, %0;" ::"r"(kConsumers) : "memory");
     if constexpr (PEER) {
@@ -515,6 +534,7 @@ struct Variant {
     void *peer[2];  // upwind, centred with the fused halo-row stores
     void *band[2];      // upwind, centred under the BAND schedule
     void *peer_band[2];  // the same with the fused halo-row stores (row strips)
+    void *load_probe[5];  // flux_op 90..94 (producer-warp level-pair variants only)
 };
 
 template <int TI, int TJ, int KC, int STAGES, int LV = 16, int LP = 1, bool WS = false>
@@ -534,6 +554,14 @@ static Variant make_variant() {
     v.peer[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND, true, false, WS>;
     v.peer[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED, true, false, WS>;
     v.band[0] = v.band[1] = v.peer_band[0] = v.peer_band[1] = nullptr;
+    for (int q = 0; q < 5; ++q) v.load_probe[q] = nullptr;
+    if constexpr (LP == 2 && WS) {
+        v.load_probe[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, kLoadProbe, false, false, WS>;
+        v.load_probe[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, kLoadProbe + 1, false, false, WS>;
+        v.load_probe[2] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, kLoadProbe + 2, false, false, WS>;
+        v.load_probe[3] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, kLoadProbe + 3, false, false, WS>;
+        v.load_probe[4] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, kLoadProbeAll, false, false, WS>;
+    }
     if constexpr (LP == 2) {  // the level-pair variants only (the default and its kin)
         v.band[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND, false, true, WS>;
         v.band[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED, false, true, WS>;
@@ -584,6 +612,7 @@ static constexpr int kCompactVariant = 21, kTallVariant = 19;
 constexpr int kGraphMinSteps = 4;  // tsg_mpdata_run replays a captured two-step graph from here
 constexpr double kReuseUnits = 8.0;
 static int g_variant = 0;  // 0 = choose per launch (pick_variant)
+static uint64_t *g_trace = nullptr;  // debug trace buffer of the next prepared launches
 
 // The BAND schedule for patches whose tile above is evicted under the contiguous schedule
 // (O1280, 2560x2576x137: 9.56-9.65 ms vs 10.13 ms with the tall tile, same box; DRAM
@@ -751,6 +780,7 @@ struct LaunchKey {
     const void *p[9];  // pd, vn, wn, rho, signs, dual, pd_out, halo_up, halo_down
     double dt, pivbz;
     int flux_op, row_lo, row_hi, variant, band;
+    const void *trace;
     bool operator==(const LaunchKey &o) const { return !memcmp(this, &o, sizeof(*this)); }
 };
 
@@ -788,6 +818,7 @@ static int prepare(tsg_grid *g, const double *pd, const double *vn, const double
     k.row_hi = row_hi;
     k.variant = g_variant;
     k.band = g_band;
+    k.trace = g_trace;
     LaunchCache *c = static_cast<LaunchCache *>(g->launches);
     if (c) {
         for (int q = 0; q < c->used; ++q)
@@ -826,8 +857,9 @@ static int prepare_uncached(tsg_grid *g, const double *pd, const double *vn, con
         return fail(TSG_EVALUE, "row range [%d, %d) outside [0, %d)", row_lo, row_hi, g->rows);
     const int K = g->levels;
     if (K < 2) return fail(TSG_EVALUE, "the transport step needs at least 2 levels, got %d", K);
+    const bool load_probe = flux_op >= kLoadProbe && flux_op <= kLoadProbeAll;
     if (flux_op != TSG_UPWIND && flux_op != TSG_CENTRED && flux_op != kProbeOp &&
-        flux_op != kComputeProbe)
+        flux_op != kComputeProbe && !load_probe)
         return fail(TSG_EVALUE, "flux operator must be one of ['centred', 'upwind'], got %d", flux_op);
     if (!pd || !vn || !wn || !rho || !signs || !dual || !pd_out)
         return fail(TSG_EVALUE, "tsg_mpdata_step: NULL array");
@@ -895,10 +927,13 @@ static int prepare_uncached(tsg_grid *g, const double *pd, const double *vn, con
     if (a.units >= (1LL << 31)) return fail(TSG_EVALUE, "patch too large for one fused launch");
 
     const bool peer = halo_up || halo_down;
-    if (peer && (flux_op == kProbeOp || flux_op == kComputeProbe))
+    if (peer && (flux_op == kProbeOp || flux_op == kComputeProbe || load_probe))
         return fail(TSG_EVALUE, "the probes do not exchange halo rows");
     L->fn = peer ? v.peer[flux_op]
+                 : load_probe ? v.load_probe[flux_op - kLoadProbe]
                  : v.fn[flux_op == kProbeOp ? 2 : (flux_op == kComputeProbe ? 3 : flux_op)];
+    if (!L->fn) return fail(TSG_EVALUE, "fused variant %d has no load probes", vi);
+    a.trace = g_trace;
     // the BAND schedule: single-GPU launches of a patch whose tile above is evicted under the
     // contiguous schedule, when every CTA gets many tiles (the deal is whole tiles)
     const bool band = !peer && flux_op <= TSG_CENTRED && v.band[0] && band_enabled() &&
@@ -1094,7 +1129,7 @@ extern "C" int tsg_mpdata_run(tsg_grid *g, double *pd_a, double *pd_b, const dou
                               tsg_stream s) {
     if (!g) return fail(TSG_EVALUE, "grid is NULL");
     if (nsteps < 0) return fail(TSG_EVALUE, "nsteps must be >= 0, got %d", nsteps);
-    if (flux_op == kProbeOp || flux_op == kComputeProbe)
+    if (flux_op != TSG_UPWIND && flux_op != TSG_CENTRED)
         return fail(TSG_EVALUE, "flux operator must be one of ['centred', 'upwind'], got %d", flux_op);
     if (nsteps == 0) return TSG_OK;
     FusedLaunch fwd, bwd;  // a -> b and b -> a
@@ -1147,6 +1182,11 @@ extern "C" int tsg_mpdata_run_strip(tsg_grid *g, double *pd_a, double *pd_b, con
 }
 
 extern "C" int tsg_time_loop_graphs_built(void) { return g_graph_builds; }
+
+extern "C" int tsg_debug_trace(uint64_t *per_cta4) {
+    g_trace = per_cta4;  // NULL switches the trace off
+    return TSG_OK;
+}
 
 extern "C" int tsg_launch_cache_stats(const tsg_grid *g, int64_t *hits, int64_t *misses) {
     if (!g) return fail(TSG_EVALUE, "grid is NULL");
