@@ -13,8 +13,10 @@
  *  - Device pointers are caller-owned (the library never allocates per call); a
  *    `tsg_stream` is a cudaStream_t, every launch is stream-ordered and asynchronous.
  *  - Thread safety: calls are reentrant across grid handles; one grid handle is used by
- *    one host thread at a time (it caches the time loops' captured graph).  The tuning
- *    switches (tsg_set_fused_variant / _band) are process-wide benchmarking hooks.
+ *    one host thread at a time (it caches the time loops' captured graph), and its fused
+ *    launches are stream-ordered (they share the handle's work-deal counters: concurrent
+ *    fused steps on one handle from two streams need two handles).  The tuning switches
+ *    (tsg_set_fused_variant / _band / _schedule) are process-wide benchmarking hooks.
  *  - Structured ("direct") fields live in the device layout
  *        double field[rows + 2][colors][cols + 2][tsg_inner_pitch(inner)]
  *    i.e. (row, colour, column) parallelogram indexing with a one-element periodic
@@ -214,6 +216,16 @@ int tsg_fused_variant_of(const tsg_grid *g, int row_lo, int row_hi);
 int tsg_fused_band_of(const tsg_grid *g, int row_lo, int row_hi);
 /* Enable (1, default) or disable (0) that band schedule. */
 int tsg_set_fused_band(int on);
+/* Scheduling of the fused launches: 0 (the default) deals the units of the producer-warp
+ * level-pair variants dynamically (a global ticket: whole tiles, the tail unit by unit)
+ * and runs tsg_mpdata_run's loop as persistent multi-step launches with per-tile step
+ * counters; 1 = the static per-CTA ranges / band deal and the captured two-step graph.
+ * A benchmarking hook like the two above.  No reference counterpart (executors.py:266-316
+ * deals tiles to a thread pool). */
+int tsg_set_fused_schedule(int sched);
+/* Reads and clears the grid's dependency-wait error word: 2 when a persistent multi-step
+ * launch timed out waiting for a neighbour tile (results of that launch are invalid). */
+int tsg_fused_wait_error(tsg_grid *g, int *err);
 
 /* ---- neighbour reductions (stencil.py:401-408; kernels.py:27-104; reference.py:137-157) */
 /* Structured ("direct") reduce for any of the 9 relations (connectivity.py:36-68):

@@ -38,142 +38,9 @@
 #include <new>
 #include <unordered_map>
 
-#include "tsg_tma.cuh"
+#include "mpdata_common.cuh"
 
 namespace tsg {
-
-// streaming (evict-first) 16-byte store: the step's output is not re-read by this launch
-__device__ __forceinline__ void stcs2(double *p, double2 v) { __stcs(reinterpret_cast<double2 *>(p), v); }
-
-// ---- tile geometry --------------------------------------------------------------------
-
-template <int TI, int TJ, int KC, int STAGES, int LV, int LP = 1>
-struct FusedCfg {
-    static constexpr int kThreads = TI * TJ * LV;                  // LV lanes per vertex
-    static constexpr int kLevelsPerThread = (KC + LV - 1) / LV;  // last pass may be partial
-    static constexpr int kPdBytes = (TI + 2) * (TJ + 2) * (KC + 4) * 8;
-    static constexpr int kVnBytes = (TI + 1) * 3 * (TJ + 1) * KC * 8;
-    static constexpr int kWnBytes = TI * TJ * (KC + 2) * 8;
-    static constexpr int kRhoBytes = TI * TJ * KC * 8;
-    static constexpr int align(int b) { return (b + 127) / 128 * 128; }
-    static constexpr int kPdOff = 0;
-    static constexpr int kVnOff = kPdOff + align(kPdBytes);
-    static constexpr int kWnOff = kVnOff + align(kVnBytes);
-    static constexpr int kRhoOff = kWnOff + align(kWnBytes);
-    static constexpr int kStageBytes = kRhoOff + align(kRhoBytes);
-    static constexpr uint32_t kTxBytes = kPdBytes + kVnBytes + kWnBytes + kRhoBytes;
-    static constexpr int kSmemBytes = STAGES * kStageBytes + 128;  // + barriers
-    static_assert(KC % 16 == 0, "KC must be a multiple of 16");
-    static_assert((LP == 1 && (LV == 16 || LV == 32)) || (LP == 2 && LV * 2 == KC),
-                  "a half-warp or a warp per vertex, or level pairs covering the chunk");
-    static_assert(((KC + 2) * 8) % 16 == 0 && (KC * 8) % 16 == 0, "TMA inner box must be 16B multiple");
-    static_assert(TI + 2 <= 256 && TJ + 2 <= 256 && KC + 4 <= 256, "TMA box <= 256");
-};
-
-// flux_op value of the data-movement probe (benchmarking the TMA pipeline alone)
-constexpr int kProbeOp = 99;
-// flux_op value of the compute probe (arithmetic on unloaded shared memory, no TMA)
-constexpr int kComputeProbe = 98;
-// flux_op values of the load probes (attribution of DRAM traffic and time per field): the
-// TMA pipeline with only pd (90), vn (91), wn (92) or rho (93) loaded, or all four (94),
-// and no arithmetic and no stores
-constexpr int kLoadProbe = 90, kLoadProbeAll = 94;
-template <int OP> __host__ __device__ constexpr bool is_load_probe() { return OP >= kLoadProbe && OP <= kLoadProbeAll; }
-template <int OP> __host__ __device__ constexpr bool loads_field(int f) {
-    return !is_load_probe<OP>() || OP == kLoadProbeAll || OP == kLoadProbe + f;
-}
-
-struct FusedArgs {
-    const double *signs;  // vertex field, inner 6
-    const double *dual;   // vertex field, inner 1
-    double *pd_out;       // vertex field, inner K
-    int rows, cols, K;
-    int row_lo, row_hi;  // rows computed by this launch: [row_lo, row_hi)
-    int flags;
-    // fused halo exchange: the ring neighbours' halo rows (peer / IPC-mapped memory) that
-    // receive this strip's first / last row; NULL = not exchanged by this kernel
-    double *halo_up, *halo_down;
-    // single-launch strip step (tsg_mpdata_step_strip; PEER instantiation only): the tile
-    // rows touching the strip's first / last row run last (`rotate`), their producer
-    // first acquires my_flags >= wait_value (both neighbours finished the previous step),
-    // and the last CTA to finish releases wait_value + 1 into the neighbours' flag words
-    const int64_t *my_flags;
-    int64_t *flag_up, *flag_down;
-    int64_t wait_value;
-    int64_t *epoch;  // non-NULL: the step counter lives here (read at start, advanced by
-                     // the last CTA) -- launches then take no per-step argument (CUDA graphs)
-    uint64_t timeout_ns;
-    int *err, *done;
-    int rotate;
-    double dt, pivbz;
-    int tiles_i, tiles_j, chunks;
-    int64_t units;
-    // debug trace (tsg_debug_trace): per CTA {entry, first stage landed, loop end, units}
-    // in globaltimer ns, or NULL
-    uint64_t *trace;
-};
-
-// BAND schedule (large patches, single-GPU launches): whole tiles dealt round robin in
-// band-major order (bands of band_w tile columns, tile rows within a band), each CTA
-// running all chunks of its tile back to back (the per-tile state stays in registers).
-// The tiles in flight at any time are ~G consecutive tiles of that order, so the tile
-// above a tile (band_w tiles earlier) is loaded at the same time by another CTA and the
-// halo rows they share are read from DRAM once.  A separate kernel parameter: the
-// contiguous instantiations compile exactly as without it.
-// A row strip (PEER launches) bands its interior tile rows 1 .. T-2 only and deals the two
-// boundary tile rows last (row T-1, then row 0), so only the final tiles wait for the
-// neighbours' step flags.
-struct BandArgs {
-    int band_w, nb_full;
-    uint32_t full_tiles;
-    FastDiv fd_band_tiles, fd_bw, fd_bw_last;
-    int row_base, tiles_i, tiles_j;  // first banded tile row; the launch's tile grid
-    uint32_t banded;                 // tiles in the band order (the rest: boundary rows)
-};
-
-__device__ __forceinline__ void band_tile(uint32_t t, const BandArgs &b, int &ti, int &tj) {
-    if (t >= b.banded) {  // the boundary tile rows of a strip
-        const int r = (int)(t - b.banded);
-        ti = r < b.tiles_j ? b.tiles_i - 1 : 0;
-        tj = r < b.tiles_j ? r : r - b.tiles_j;
-    } else if (t < b.full_tiles) {
-        const uint32_t band = b.fd_band_tiles.div(t), r = t - band * b.fd_band_tiles.d;
-        const uint32_t row = b.fd_bw.div(r);
-        ti = b.row_base + (int)row;
-        tj = (int)(band * b.band_w + (r - row * b.fd_bw.d));
-    } else {
-        const uint32_t r = t - b.full_tiles, row = b.fd_bw_last.div(r);
-        ti = b.row_base + (int)row;
-        tj = b.nb_full * b.band_w + (int)(r - row * b.fd_bw_last.d);
-    }
-}
-
-__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
-    int64_t v;
-    asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ uint64_t globaltimer_ns() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-// spin (with back-off) until both flag words reach `value`; on timeout report through `err`
-// and carry on, so a lost neighbour cannot hang the GPU
-__device__ inline void wait_both(const int64_t *flags, int64_t value, uint64_t timeout_ns, int *err) {
-    const uint64_t t0 = globaltimer_ns();
-    unsigned backoff = 32;
-    while (ld_acquire_sys(flags) < value || ld_acquire_sys(flags + 1) < value) {
-        if (globaltimer_ns() - t0 > timeout_ns) {
-            if (err) atomicExch(err, 1);
-            return;
-        }
-        __nanosleep(backoff);
-        if (backoff < 4096) backoff *= 2;
-    }
-}
 
 // LP: levels per thread.  LP = 1: thread per (vertex, level), LV lanes per vertex.
 // LP = 2: a thread owns the adjacent level pair (k, k+1): 16-byte shared loads and stores,
@@ -362,73 +229,8 @@ __global__ void __launch_bounds__(TI *TJ * LV + (WS ? 32 : 0), 1)
         if constexpr (LP == 2) {
             const int k = k0 + kq;  // this thread's level pair (k, k+1)
             if (!is_load_probe<OP>() && vvalid && k < a.K) {
-                const double *P = sp;
-                const double *V = sv;
-                const double2 c = ld2(P);
-                if constexpr (OP == kProbeOp) {  // data-movement probe
-                    const double2 v0 = ld2(V), w01 = ld2(sw), r = ld2(sr);
-                    st2(out + k, make_double2(add(add(c.x, v0.x), add(w01.x, r.x)),
-                                              add(add(c.y, v0.y), add(w01.y, r.y))));
-                    goto next_unit;
-                }
-                const double2 q0 = ld2(P + sPj), q1 = ld2(P + sPi + sPj), q2 = ld2(P + sPi);
-                const double2 q3 = ld2(P - sPj), q4 = ld2(P - sPi - sPj), q5 = ld2(P - sPi);
-                const double2 v0 = ld2(V), v1 = ld2(V + sVc), v2 = ld2(V + 2 * sVc);
-                const double2 v3 = ld2(V - KC), v4 = ld2(V - sVi + sVc - KC), v5 = ld2(V - sVi + 2 * sVc);
-                const double pm = P[-1], pp = P[2];
-                const double2 w01 = ld2(sw);
-                const double w2 = sw[2];
-                const double2 r = ld2(sr);
-                // interfaces k, k+1, k+2 (reference.py:38-60); k+1 is shared by the pair
-                double z0 = fluz_interior(w01.x, pm, c.x);
-                const double z1 = fluz_interior(w01.y, c.x, c.y);
-                double z2 = fluz_interior(w2, c.y, pp);
-                if (chunk == 0 && k == 0) z0 = mul(a.pivbz, z1);
-                const bool pair = k + 1 < a.K;
-                if (chunk == last_chunk && k + 1 == a.K - 1) z2 = mul(a.pivbz, z1);
-                const double z1a = pair ? z1 : mul(a.pivbz, z0);  // k is the top level
-                double acc = 0.0, acd = 0.0;
-                acc = add(mul(sg0, edge_flux<OP>(c.x, q0.x, v0.x)), acc);
-                acd = add(mul(sg0, edge_flux<OP>(c.y, q0.y, v0.y)), acd);
-                acc = add(mul(sg1, edge_flux<OP>(c.x, q1.x, v1.x)), acc);
-                acd = add(mul(sg1, edge_flux<OP>(c.y, q1.y, v1.y)), acd);
-                acc = add(mul(sg2, edge_flux<OP>(c.x, q2.x, v2.x)), acc);
-                acd = add(mul(sg2, edge_flux<OP>(c.y, q2.y, v2.y)), acd);
-                acc = add(mul(sg3, edge_flux<OP>(q3.x, c.x, v3.x)), acc);
-                acd = add(mul(sg3, edge_flux<OP>(q3.y, c.y, v3.y)), acd);
-                acc = add(mul(sg4, edge_flux<OP>(q4.x, c.x, v4.x)), acc);
-                acd = add(mul(sg4, edge_flux<OP>(q4.y, c.y, v4.y)), acd);
-                acc = add(mul(sg5, edge_flux<OP>(q5.x, c.x, v5.x)), acc);
-                acd = add(mul(sg5, edge_flux<OP>(q5.y, c.y, v5.y)), acd);
-                acc = add(acc, sub(z1a, z0));
-                acd = add(acd, sub(z2, z1));
-                double2 val;
-                val.x = sub(c.x, dvd(mul(a.dt, dvd(acc, dual)), r.x));
-                val.y = sub(c.y, dvd(mul(a.dt, dvd(acd, dual)), r.y));
-                double *o = out + k;
-                if (pair) {
-                    stcs2(o, val);
-                    if (d_row | d_col) {
-                        if (d_row) stcs2(o + d_row, val);
-                        if (d_col) stcs2(o + d_col, val);
-                        if (d_row && d_col) stcs2(o + d_row + d_col, val);
-                    }
-                    if (PEER && peer) {
-                        st2(peer + k, val);
-                        if (d_col) st2(peer + k + d_col, val);
-                    }
-                } else {
-                    o[0] = val.x;
-                    if (d_row | d_col) {
-                        if (d_row) o[d_row] = val.x;
-                        if (d_col) o[d_col] = val.x;
-                        if (d_row && d_col) o[d_row + d_col] = val.x;
-                    }
-                    if (PEER && peer) {
-                        peer[k] = val.x;
-                        if (d_col) peer[k + d_col] = val.x;
-                    }
-                }
+                const VertexState vs{sg0, sg1, sg2, sg3, sg4, sg5, dual, out, peer, d_row, d_col};
+                level_pair_update<TJ, KC, OP, PEER>(sp, sv, sw, sr, vs, k, a.K, a.dt, a.pivbz);
             }
         } else
 #pragma unroll
@@ -486,7 +288,6 @@ __global__ void __launch_bounds__(TI *TJ * LV + (WS ? 32 : 0), 1)
                 }
             }
         }
-    next_unit:
         if (++chunk == a.chunks) {
             chunk = 0;
             if constexpr (BAND) {
@@ -530,6 +331,7 @@ __global__ void __launch_bounds__(TI *TJ * LV + (WS ? 32 : 0), 1)
 struct Variant {
     int ti, tj, kc, stages;
     int threads, smem;
+    bool dyn_ok;    // a producer-warp level-pair variant: has a dynamically dealt counterpart
     void *fn[4];    // upwind, centred, data-movement probe, compute probe
     void *peer[2];  // upwind, centred with the fused halo-row stores
     void *band[2];      // upwind, centred under the BAND schedule
@@ -547,6 +349,7 @@ static Variant make_variant() {
     v.stages = STAGES;
     v.threads = C::kThreads + (WS ? 32 : 0);
     v.smem = C::kSmemBytes;
+    v.dyn_ok = WS && LP == 2 && dyn_shape(TI, TJ, KC, STAGES) != nullptr;
     v.fn[0] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_UPWIND, false, false, WS>;
     v.fn[1] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, TSG_CENTRED, false, false, WS>;
     v.fn[2] = (void *)mpdata_fused_kernel<TI, TJ, KC, STAGES, LV, LP, kProbeOp, false, false, WS>;
@@ -612,6 +415,9 @@ static constexpr int kCompactVariant = 21, kTallVariant = 19;
 constexpr int kGraphMinSteps = 4;  // tsg_mpdata_run replays a captured two-step graph from here
 constexpr double kReuseUnits = 8.0;
 static int g_variant = 0;  // 0 = choose per launch (pick_variant)
+// 0 = dynamic deal (mpdata_dyn.cu) wherever the chosen variant has one, 1 = the static
+// contiguous / band schedule of this file (tsg_set_fused_schedule)
+static int g_sched = 0;
 static uint64_t *g_trace = nullptr;  // debug trace buffer of the next prepared launches
 
 // The BAND schedule for patches whose tile above is evicted under the contiguous schedule
@@ -635,7 +441,7 @@ constexpr int kBandTiles = 16;  // BAND schedule: tile columns per band
 // band-major order of a launch's tiles; a strip bands rows 1 .. T-2 and deals its two
 // boundary tile rows last
 static void fill_band(BandArgs &b, int tiles_i, int tiles_j, bool strip) {
-    const int rows = strip ? tiles_i - 2 : tiles_i;
+    const int rows = strip ? std::max(tiles_i - 2, 0) : tiles_i;
     b.row_base = strip ? 1 : 0;
     b.tiles_i = tiles_i;
     b.tiles_j = tiles_j;
@@ -686,6 +492,12 @@ extern "C" int tsg_fused_variant_info(int variant, int *ti, int *tj, int *kc, in
     if (stages) *stages = v.stages;
     if (threads) *threads = v.threads;
     if (smem_bytes) *smem_bytes = v.smem;
+    return TSG_OK;
+}
+
+extern "C" int tsg_set_fused_schedule(int sched) {
+    if (sched != 0 && sched != 1) return fail(TSG_EVALUE, "fused schedule must be 0 (dynamic) or 1 (static), got %d", sched);
+    g_sched = sched;
     return TSG_OK;
 }
 
@@ -743,11 +555,44 @@ extern "C" int tsg_mpdata_step_rows(tsg_grid *g, const double *pd, const double 
 // the grid, so a time loop encodes its maps once (tsg_mpdata_run).
 struct FusedLaunch {
     CUtensorMap m_pd, m_vn, m_wn, m_rho;
+    CUtensorMap m_pd_alt;  // dyn multi-step: the odd steps' input (the even steps' output)
     FusedArgs a;
     BandArgs ba;
+    DynArgs d;
     void *fn;
     int grid, threads, smem;
+    bool dyn, coop;  // the dynamically dealt kernel; launched cooperatively (co-residency)
 };
+
+// ---- device workspace of the dynamically dealt launches ----------------------------------
+// [0, 128): kLaunchCacheSize ticket slots of 4 words (one per cached launch, so launches
+// with different arguments never share a ticket); [128]: the tile counters' base (u64);
+// [136]: the dependency-wait error word; [256, ...): one u64 counter per tile.
+constexpr int kDynHeader = 256, kDynBaseOff = 128, kDynErrOff = 136;
+
+int tsg::create_dyn_workspace(tsg_grid *g) {
+    // tile counters for the smallest dynamically dealt tile (4 x 12)
+    const int64_t tiles = (int64_t)((g->rows + 3) / 4) * ((g->cols + 11) / 12);
+    const size_t bytes = kDynHeader + (size_t)tiles * 8;
+    void *p = nullptr;
+    TSG_CHECK_CUDA(cudaMalloc(&p, bytes));
+    if (cudaMemset(p, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+        cudaFree(p);
+        return fail(TSG_ECUDA, "dyn workspace initialisation failed");
+    }
+    g->dyn_ws = p;
+    g->dyn_tiles = tiles;
+    return TSG_OK;
+}
+
+void tsg::destroy_dyn_workspace(tsg_grid *g) {
+    if (g->dyn_ws) cudaFree(g->dyn_ws);
+    g->dyn_ws = nullptr;
+}
+
+static uint32_t *dyn_ticket(const tsg_grid *g, int slot) {
+    return reinterpret_cast<uint32_t *>(static_cast<unsigned char *>(g->dyn_ws)) + 4 * slot;
+}
 
 static int encode_pd(const Variant &v, const tsg_grid *g, const double *pd, CUtensorMap *m) {
     const cuuint64_t pv = (cuuint64_t)pitch_of(g->levels);
@@ -802,6 +647,20 @@ static int prepare_uncached(tsg_grid *g, const double *pd, const double *vn, con
                             double *pd_out, double dt, double pivbz, int flux_op, int row_lo,
                             int row_hi, double *halo_up, double *halo_down, FusedLaunch *L);
 
+// Items of a dynamically dealt launch of `nsteps` steps: whole tiles, except that the last
+// step's final ~two rounds of the grid go out one unit at a time (balanced tail).
+static void set_dyn_items(FusedLaunch *L, int nsteps) {
+    DynArgs &d = L->d;
+    const uint32_t T = (uint32_t)L->a.tiles_i * (uint32_t)L->a.tiles_j, C = (uint32_t)L->a.chunks;
+    const uint32_t tail = (2u * (uint32_t)L->grid + C - 1) / C;  // tiles dealt unit by unit
+    d.nsteps = nsteps;
+    d.tiles = T;
+    d.whole = T > tail ? T - tail : 0;
+    d.items = (uint32_t)(nsteps - 1) * T + d.whole + (T - d.whole) * C;
+    d.fd_tiles = FastDiv(T);
+    d.fd_chunks = FastDiv(C);
+}
+
 static int prepare(tsg_grid *g, const double *pd, const double *vn, const double *wn,
                    const double *rho, const double *signs, const double *dual, double *pd_out,
                    double dt, double pivbz, int flux_op, int row_lo, int row_hi, double *halo_up,
@@ -817,7 +676,7 @@ static int prepare(tsg_grid *g, const double *pd, const double *vn, const double
     k.row_lo = row_lo;
     k.row_hi = row_hi;
     k.variant = g_variant;
-    k.band = g_band;
+    k.band = g_band + 2 * g_sched;
     k.trace = g_trace;
     LaunchCache *c = static_cast<LaunchCache *>(g->launches);
     if (c) {
@@ -833,10 +692,11 @@ static int prepare(tsg_grid *g, const double *pd, const double *vn, const double
         return rc;
     if (!c) {
         c = new (std::nothrow) LaunchCache;
-        if (!c) return TSG_OK;  // no cache: correct, just slower
+        if (!c) return TSG_OK;  // no cache: correct, just slower (ticket slot 0)
         g->launches = c;
     }
     const int slot = c->next;
+    if (L->dyn) L->d.ticket = dyn_ticket(g, slot);
     c->next = (c->next + 1) % kLaunchCacheSize;
     if (c->used < kLaunchCacheSize) ++c->used;
     c->key[slot] = k;
@@ -892,10 +752,14 @@ static int prepare_uncached(tsg_grid *g, const double *pd, const double *vn, con
         if (int rc = make_map(&L->m_vn, vn, 4, dims, str, box)) return rc;
     }
     {
-        cuuint64_t dims[3] = {(cuuint64_t)K + 1, W, H};
+        // extent K, not K + 1: the top interface wn(K) is never read (fluz(K) = pivbz *
+        // fluz(K-1), reference.py:38-60), so the last chunk's box ends at level K-1 and,
+        // with 128-byte promotion, its DRAM fetch stops at the end of the used run instead
+        // of pulling in the pitch padding (pitch_of(K+1) = 96 at K = 80: 15 % of the field)
+        cuuint64_t dims[3] = {(cuuint64_t)K, W, H};
         cuuint64_t str[2] = {pw * 8, W * pw * 8};
         cuuint32_t box[3] = {(cuuint32_t)v.kc + 2, (cuuint32_t)v.tj, (cuuint32_t)v.ti};
-        if (int rc = make_map(&L->m_wn, wn, 3, dims, str, box)) return rc;
+        if (int rc = make_map(&L->m_wn, wn, 3, dims, str, box, CU_TENSOR_MAP_L2_PROMOTION_L2_128B)) return rc;
     }
 
     FusedArgs &a = L->a;
@@ -944,6 +808,31 @@ static int prepare_uncached(tsg_grid *g, const double *pd, const double *vn, con
         L->fn = v.band[flux_op];
         fill_band(L->ba, tiles_i, a.tiles_j, false);
     }
+    // the dynamic deal (mpdata_dyn.cu) for the producer-warp level-pair variants
+    const DynShape *ds = nullptr;
+    if (g_sched == 0 && v.dyn_ok && g->dyn_ws && (flux_op <= TSG_CENTRED || (flux_op == kProbeOp && !peer)))
+        ds = dyn_shape(v.ti, v.tj, v.kc, v.stages);
+    if (ds) {
+        L->dyn = true;
+        L->fn = ds->fn[peer ? 1 : 0][flux_op == kProbeOp ? 2 : flux_op];
+        fill_band(L->ba, tiles_i, a.tiles_j, peer);  // a strip deals its boundary tile rows last
+        DynArgs &d = L->d;
+        d.ticket = dyn_ticket(g, 0);
+        d.tile_done = reinterpret_cast<uint64_t *>(static_cast<unsigned char *>(g->dyn_ws) + kDynHeader);
+        d.base = reinterpret_cast<uint64_t *>(static_cast<unsigned char *>(g->dyn_ws) + kDynBaseOff);
+        d.err = reinterpret_cast<int *>(static_cast<unsigned char *>(g->dyn_ws) + kDynErrOff);
+        d.timeout_ns = 20ull * 1000000000ull;
+        d.pd_alt = nullptr;
+        if (int rc = set_smem_once(L->fn, ds->smem)) return rc;
+        int per_sm = 0;
+        TSG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L->fn, ds->threads, ds->smem));
+        if (per_sm < 1) return fail(TSG_ECUDA, "dynamic fused variant %d does not fit on an SM", vi);
+        L->grid = g->num_sms * per_sm;
+        L->threads = ds->threads;
+        L->smem = ds->smem;
+        set_dyn_items(L, 1);
+        return TSG_OK;
+    }
     if (int rc = set_smem_once(L->fn, v.smem)) return rc;
     int per_sm = 0;
     TSG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L->fn, v.threads, v.smem));
@@ -958,6 +847,16 @@ static int prepare_uncached(tsg_grid *g, const double *pd, const double *vn, con
 
 static int launch(FusedLaunch *L, tsg_stream s) {
     if (L->a.units == 0) return TSG_OK;
+    if (L->dyn) {
+        void *args[] = {&L->m_pd, &L->m_pd_alt, &L->m_vn, &L->m_wn, &L->m_rho, &L->a, &L->ba, &L->d};
+        if (L->coop)
+            TSG_CHECK_CUDA(cudaLaunchCooperativeKernel(L->fn, dim3((unsigned)L->grid), dim3(L->threads), args,
+                                                       L->smem, (cudaStream_t)s));
+        else
+            TSG_CHECK_CUDA(cudaLaunchKernel(L->fn, dim3((unsigned)L->grid), dim3(L->threads), args, L->smem,
+                                            (cudaStream_t)s));
+        return TSG_OK;
+    }
     void *args[] = {&L->m_pd, &L->m_vn, &L->m_wn, &L->m_rho, &L->a, &L->ba};
     TSG_CHECK_CUDA(cudaLaunchKernel(L->fn, dim3((unsigned)L->grid), dim3(L->threads), args, L->smem,
                                     (cudaStream_t)s));
@@ -1004,7 +903,7 @@ static int prepare_strip(tsg_grid *g, const double *pd, const double *vn, const 
     int n = 0;
     const int vi = pick_variant(g, g->rows);
     const Variant &v = variants(&n)[vi - 1];
-    if (v.peer_band[0] && band_enabled() && evicted(g, g->rows) && a.tiles_i >= 3 &&
+    if (!L->dyn && v.peer_band[0] && band_enabled() && evicted(g, g->rows) && a.tiles_i >= 3 &&
         (int64_t)a.tiles_i * a.tiles_j >= 16LL * g->num_sms && flux_op <= TSG_CENTRED) {
         L->fn = v.peer_band[flux_op];
         if (int rc = set_smem_once(L->fn, v.smem)) return rc;
@@ -1039,7 +938,7 @@ static GraphKey graph_key(const void *const *ptrs, int n, double dt, double pivb
     k.flux_op = flux_op;
     k.timeout_ms = timeout_ms;
     k.variant = g_variant;
-    k.band = g_band;
+    k.band = g_band + 2 * g_sched;
     return k;
 }
 
@@ -1136,6 +1035,39 @@ extern "C" int tsg_mpdata_run(tsg_grid *g, double *pd_a, double *pd_b, const dou
     if (int rc = prepare(g, pd_a, vn, wn, rho, signs, dual, pd_b, dt, pivbz, flux_op, 0, g->rows,
                          nullptr, nullptr, &fwd))
         return rc;
+    if (fwd.dyn && nsteps >= 2) {  // the whole loop in persistent multi-step launches
+        int n = 0;
+        const Variant &v = variants(&n)[pick_variant(g, g->rows) - 1];
+        const DynShape *ds = dyn_shape(v.ti, v.tj, v.kc, v.stages);
+        if (ds && (int64_t)fwd.a.tiles_i * fwd.a.tiles_j <= g->dyn_tiles) {
+            FusedLaunch M = fwd;
+            M.fn = ds->fn[2][flux_op];
+            M.coop = true;
+            M.threads = ds->multi_threads;
+            if (int rc = set_smem_once(M.fn, ds->smem)) return rc;
+            if (int rc = encode_pd(v, g, pd_b, &M.m_pd_alt)) return rc;
+            M.d.pd_alt = pd_a;
+            const int64_t T = (int64_t)fwd.a.tiles_i * fwd.a.tiles_j;
+            // items per launch < 2^31; an even step count per launch keeps a -> b parity
+            int64_t smax = ((int64_t)1 << 30) / (T * fwd.a.chunks);
+            smax = smax < 2 ? 2 : (smax & ~(int64_t)1);
+            bool ab = true;
+            for (int left = nsteps; left > 0;) {
+                const int S = (int)(left < smax ? left : smax);
+                FusedLaunch X = M;
+                if (!ab) {
+                    std::swap(X.m_pd, X.m_pd_alt);
+                    X.a.pd_out = pd_a;
+                    X.d.pd_alt = pd_b;
+                }
+                set_dyn_items(&X, S);
+                if (int rc = launch(&X, s)) return rc;
+                if (S % 2) ab = !ab;
+                left -= S;
+            }
+            return TSG_OK;
+        }
+    }
     bwd = fwd;
     bwd.a.pd_out = pd_a;
     {
@@ -1185,6 +1117,16 @@ extern "C" int tsg_time_loop_graphs_built(void) { return g_graph_builds; }
 
 extern "C" int tsg_debug_trace(uint64_t *per_cta4) {
     g_trace = per_cta4;  // NULL switches the trace off
+    return TSG_OK;
+}
+
+extern "C" int tsg_fused_wait_error(tsg_grid *g, int *err) {
+    if (!g || !err) return fail(TSG_EVALUE, "grid or err is NULL");
+    *err = 0;
+    if (!g->dyn_ws) return TSG_OK;
+    int *w = reinterpret_cast<int *>(static_cast<unsigned char *>(g->dyn_ws) + kDynErrOff);
+    TSG_CHECK_CUDA(cudaMemcpy(err, w, sizeof(int), cudaMemcpyDeviceToHost));
+    TSG_CHECK_CUDA(cudaMemset(w, 0, sizeof(int)));
     return TSG_OK;
 }
 

@@ -54,6 +54,12 @@ extern "C" int tsg_grid_create(int rows, int cols, int levels, int flags, tsg_gr
     g->num_sms = sms;
     g->graph = nullptr;
     g->launches = nullptr;
+    g->dyn_ws = nullptr;
+    g->dyn_tiles = 0;
+    if (int rc = tsg::create_dyn_workspace(g)) {
+        delete g;
+        return rc;
+    }
     *out = g;
     tsg::clear_error();
     return TSG_OK;
@@ -73,6 +79,7 @@ extern "C" int tsg_grid_destroy(tsg_grid *g) {
     if (g) {
         tsg::destroy_graph_cache(g);
         tsg::destroy_launch_cache(g);
+        tsg::destroy_dyn_workspace(g);
     }
     delete g;
     return TSG_OK;

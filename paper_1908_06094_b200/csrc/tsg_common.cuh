@@ -18,11 +18,16 @@ struct tsg_grid {
     void *graph;  // cached two-step CUDA graph of the time loops (mpdata_fused.cu), or NULL
     void *launches;  // prepared fused launches (tensor maps, arguments, grid) keyed by their
                      // arguments (mpdata_fused.cu), or NULL
+    void *dyn_ws;    // device workspace of the dynamically dealt fused launches: ticket words,
+                     // tile counters of the multi-step loop (mpdata_fused.cu), or NULL
+    int64_t dyn_tiles;  // tile counters in dyn_ws
 };
 
 namespace tsg {
 void destroy_graph_cache(tsg_grid *g);
 void destroy_launch_cache(tsg_grid *g);
+int create_dyn_workspace(tsg_grid *g);
+void destroy_dyn_workspace(tsg_grid *g);
 }
 
 namespace tsg {

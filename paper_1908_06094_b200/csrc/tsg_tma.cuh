@@ -92,13 +92,14 @@ inline int get_encode() {
 }
 
 inline int make_map(CUtensorMap *m, const double *ptr, int rank, const cuuint64_t *dims,
-                    const cuuint64_t *strides_bytes, const cuuint32_t *box) {
+                    const cuuint64_t *strides_bytes, const cuuint32_t *box,
+                    CUtensorMapL2promotion promotion = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
     cuuint32_t es[4] = {1, 1, 1, 1};
     if (reinterpret_cast<uintptr_t>(ptr) % 16)
         return fail(TSG_EVALUE, "field base address must be 16-byte aligned for TMA");
     CUresult r = tma_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double *>(ptr), dims,
                           strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, promotion,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(TSG_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return TSG_OK;

@@ -26,6 +26,7 @@ ap.add_argument("shape", nargs="?", default="279x256x80")
 ap.add_argument("--ops", default="0,99,98,94,90,91,92,93")
 ap.add_argument("--reps", type=int, default=50)
 ap.add_argument("--variant", type=int, default=0)
+ap.add_argument("--sched", type=int, default=0, help="0 dynamic deal (default), 1 static ranges")
 ap.add_argument("--out", default=None)
 a = ap.parse_args()
 shape = tuple(int(x) for x in a.shape.split("x"))
@@ -35,6 +36,7 @@ st.set_geometry(inp["signs"], inp["dual"])
 st.upload(inp["pd"], inp["vn"], inp["wn"], inp["rho"])
 if a.variant:
     _lib.call("tsg_set_fused_variant", a.variant)
+_lib.call("tsg_set_fused_schedule", a.sched)
 flush = torch.ones(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
 sink = torch.empty(1, dtype=torch.float64, device="cuda")
 B = mpdata_algorithmic_bytes(*shape)

@@ -1,18 +1,27 @@
-"""Back-to-back fused time loop (tsg_mpdata_run, no L2 flush between steps) vs flushed single
-steps at 279x256x80 -- how much of the per-step time is launch ramp / L2 effects."""
+"""Back-to-back fused time loop (tsg_mpdata_run, no L2 flush between steps) at 279x256x80
+(or RxCxK), for each work deal: schedule 1 = static ranges + captured two-step graph,
+0 = dynamic deal + persistent multi-step launches.
+    python tools/time_loop.py [RxCxK] [--sched 0,1]"""
+import argparse
 import sys
 sys.path.insert(0, "/root/repo")
 import torch
-from paper_1908_06094_b200 import PatchSpec, StructuredStepper
+from paper_1908_06094_b200 import PatchSpec, StructuredStepper, _lib
 from paper_1908_06094_b200.workloads import transport_inputs, mpdata_algorithmic_bytes
 
-shape = tuple(int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "279x256x80").split("x"))
+ap = argparse.ArgumentParser()
+ap.add_argument("shape", nargs="?", default="279x256x80")
+ap.add_argument("--sched", default="1,0")
+ap.add_argument("--n", default="1,10,100,1000")
+args = ap.parse_args()
+shape = tuple(int(x) for x in args.shape.split("x"))
 inp = transport_inputs(*shape)
 st = StructuredStepper(PatchSpec(*shape))
 st.set_geometry(inp["signs"], inp["dual"])
 st.upload(inp["pd"], inp["vn"], inp["wn"], inp["rho"])
 B = mpdata_algorithmic_bytes(*shape)
-for n in (1, 10, 100, 1000):
+for sched, n in [(int(q), int(m)) for q in args.sched.split(",") for m in args.n.split(",")]:
+    _lib.call("tsg_set_fused_schedule", sched)
     st.run(n, 0.1, 1.0)
     torch.cuda.synchronize()
     ts = []
@@ -22,4 +31,4 @@ for n in (1, 10, 100, 1000):
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) / n)
     t = min(ts) * 1e-3
-    print(f"run({n:4d}): {t*1e6:.1f} us/step  {B/t/1e9:.0f} GB/s")
+    print(f"sched {sched} run({n:4d}): {t*1e6:.1f} us/step  {B/t/1e9:.0f} GB/s", flush=True)
