@@ -13,9 +13,16 @@ U[-0.5,0.5) velocities, rho = 1, uniform geometry, dt = 0.1, pivbz = 1).
   HBM, every rank stepping its 279-row strip of a (279*N) x 256 x 80 patch
   through ``StripStepper`` (N = 1: the periodic patch; N > 1: row strips with
   the per-step halo exchange) -- the same code path and the same per-strip
-  inputs at every N (weak scaling).  Each timed step is bracketed by CUDA events
-  on the launching stream, preceded (outside the events) by a 256 MiB L2 flush
-  and a short device sleep that keeps the host's launches ahead of the GPU.
+  inputs at every N (weak scaling).  The timed region is the reference's time
+  loop (bench.py:398-403): K dependent steps, each consuming the previous
+  step's density (``StripStepper.run``: one persistent multi-step launch per
+  rank, halo exchange inside it for N > 1), bracketed by a barrier + device
+  synchronize and CUDA events on the launching stream; no L2 flush between the
+  steps -- every step streams 320 MB per rank through a 126 MB L2 -- and a
+  256 MiB L2 flush before the region.
+* step_flushed: the same step timed one launch at a time, each preceded
+  (outside its events) by the L2 flush: per-step spread, and the cold-cache
+  single-step figure (round 1's headline protocol).
 * o1280_strong: configs[4], the 2560 x 2576 x 137 patch cut into N strips
   through the same StripStepper path (on-device counter-hash inputs), for the
   strong-scaling efficiency T1 / (N * T_N) against the N = 1 run's record.
@@ -314,22 +321,25 @@ def o1280_strong(args, rank, world, shared, barrier, peak):
     w = WORKLOADS["o1280"]
     R, C, K = w["rows"], w["cols"], w["levels"]
     st = StripStepper(R, C, K, rank, world, seed=0, mode=args.exchange)
-    for _ in range(3):
-        st.step(DT, PIVBZ)
-        st.swap()
+    st.run(3, DT, PIVBZ)
     torch.cuda.synchronize()
     if world > 1:
         st.check()
     barrier()
-    ms = _timed_steps(st, args.o1280_steps, torch.cuda.current_stream())
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    st.run(args.o1280_steps, DT, PIVBZ)  # the dependent loop, as the headline
+    e1.record(stream)
+    torch.cuda.synchronize()
     barrier()
     if world > 1:
         st.finish()
         st.check()
-    t = _max_over_ranks(sum(ms) / 1e3, world, shared) / len(ms)
+    t = _max_over_ranks(e0.elapsed_time(e1) / 1e3, world, shared) / args.o1280_steps
     mine = mpdata_algorithmic_bytes(st.nrows, C, K)
     rec = {"value": R * C * K / t, "unit": UNIT, "n_gpus": world, "scaling": "strong",
-           "ms_per_step": t * 1e3, "step_ms": step_stats(ms), "steps": len(ms),
+           "ms_per_step": t * 1e3, "steps": args.o1280_steps,
            "config": workload_config(w, world), "rows_per_gpu": st.nrows,
            "effective_gbs": mine / t / 1e9, "roofline_frac": mine / t / 1e9 / peak,
            "path": f"StripStepper ({'periodic patch' if world == 1 else st.mode + ' exchange'})",
@@ -435,21 +445,41 @@ def run_ours(args):
         def flush_l2():
             flush_sink.copy_(flush.sum().reshape(1))
 
-        _timed_steps(stepper, args.warmup, stream, flush_l2)  # warm-up = the timed sequence
+        # warm-up: the timed loop itself (W dependent steps), then one flushed step sequence
+        stepper.run(args.warmup, DT, PIVBZ)
         if world > 1:
             stepper.check()  # a broken exchange fails here, not after every timed step has timed out
+        flush_l2()
         barrier()
         torch.cuda.synchronize()
+        barrier()
         t_wall0 = time.perf_counter()
-        step_ms = _timed_steps(stepper, args.steps, stream, flush_l2)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        stepper.run(args.steps, DT, PIVBZ)  # the timed region: K dependent steps
+        ev1.record(stream)
+        torch.cuda.synchronize()
         barrier()
         t_wall = time.perf_counter() - t_wall0
         if world > 1:
             stepper.finish()
             stepper.check()
-        total_s = _max_over_ranks(sum(step_ms) / 1e3, world, shared)
+        total_s = _max_over_ranks(ev0.elapsed_time(ev1) / 1e3, world, shared)
         mean_step = total_s / args.steps
         value = GV * K / mean_step
+        loop_launches = (_lib.lib().tsg_fused_loop_launches(stepper.grid.handle, args.steps)
+                         if world == 1 or args.exchange == "p2p" else 3 * args.steps)
+        # the flushed single-step sequence (round 1's protocol): per-step spread
+        _timed_steps(stepper, min(args.warmup, 5), stream, flush_l2)
+        if world > 1:
+            stepper.check()
+        barrier()
+        step_ms = _timed_steps(stepper, args.flushed_steps, stream, flush_l2)
+        barrier()
+        if world > 1:
+            stepper.finish()
+            stepper.check()
+        flushed_s = _max_over_ranks(sum(step_ms) / 1e3, world, shared) / len(step_ms)
         variant = _lib.lib().tsg_fused_variant_of(stepper.grid.handle, 0, my_rows)
         band = world == 1 and _lib.lib().tsg_fused_band_of(stepper.grid.handle, 0, my_rows) == 1
         hits = _lib.ctypes.c_int64()
@@ -494,19 +524,26 @@ def run_ours(args):
             e2e_all = e2e_run(pinned, "independent host-fed steps as e2e, with every input (pd / vn / "
                                       "wn / rho, the flat oracle call of reference.py:93-116) copied "
                                       "H2D per step")
-            # back-to-back device time loop (tsg_mpdata_run ping-pong, no flush: 320 MB > L2)
-            n_loop = 100
-            st.run(n_loop, DT, PIVBZ)
-            torch.cuda.synchronize()
-            l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            l0.record(stream)
-            st.run(n_loop, DT, PIVBZ)
-            l1.record(stream)
-            torch.cuda.synchronize()
+            # the same dependent loop with the static schedule (per-step launches replayed as a
+            # captured two-step graph, round 1's loop) for comparison
+            n_loop = args.steps
+            _lib.call("tsg_set_fused_schedule", 1)
+            try:
+                st.run(n_loop, DT, PIVBZ)
+                flush_l2()
+                torch.cuda.synchronize()
+                l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                l0.record(stream)
+                st.run(n_loop, DT, PIVBZ)
+                l1.record(stream)
+                torch.cuda.synchronize()
+            finally:
+                _lib.call("tsg_set_fused_schedule", 0)
             t_loop = l0.elapsed_time(l1) / 1e3 / n_loop
             loop = {"value": V * K / t_loop, "unit": UNIT, "ms_per_step": t_loop * 1e3, "steps": n_loop,
-                    "l2": "no flush: inputs (320 MB) larger than L2",
-                    "api": "StructuredStepper.run (tsg_mpdata_run, captured two-step graph)"}
+                    "roofline_frac": mpdata_algorithmic_bytes(w["rows"], cols, K) / t_loop / 1e9 / peak,
+                    "api": "StructuredStepper.run with tsg_set_fused_schedule(1): static per-CTA ranges, "
+                           "one launch per step replayed as a captured two-step CUDA graph"}
             del st
             torch.cuda.empty_cache()
             e2e_loop = e2e_time_loop(w, max(5, min(args.steps, 20)))
@@ -549,13 +586,22 @@ def run_ours(args):
                                     "neighbours' halos (CUDA IPC over NVLink), in-kernel step fence"
                                     if args.exchange == "p2p" else "NCCL grouped send/recv"),
                   **({"exchange_fallback": exchange_note} if exchange_note else {}),
-                  "l2": "256 MiB read-only L2 flush before every timed step (outside the events)",
-                  "fused_schedule": ("band round robin" if band else "contiguous ranges"),
+                  "l2": "no flush between the timed loop's steps (each streams 320 MB per rank through "
+                        "the 126 MB L2); a 256 MiB read-only L2 flush before the timed region",
+                  "timed_region": f"StripStepper.run({args.steps}): {args.steps} dependent steps (the "
+                                  "reference's time loop, bench.py:398-403) in "
+                                  f"{loop_launches} persistent launch(es) per rank",
+                  "fused_schedule": "dynamic deal (global ticket: whole tiles in "
+                                    + ("band" if band else "tile-major") + " order, the tail unit by "
+                                    "unit); steps chained by per-tile step counters",
                   "fused_tile": {"variant": variant, "ti": vi[0].value, "tj": vi[1].value, "kc": vi[2].value,
                                  "stages": vi[3].value, "threads": vi[4].value, "smem_bytes": vi[5].value},
                   "launch_cache": {"hits": hits.value, "misses": misses.value}},
-        "step_ms": step_stats(step_ms),
-        **({"step_ms_all": [round(x, 5) for x in step_ms]} if len(step_ms) <= 64 else {}),
+        "step_flushed": {
+            "value": GV * K / flushed_s, "unit": UNIT, "ms_per_step": flushed_s * 1e3,
+            "roofline_frac": bcomp / flushed_s / 1e9 / peak, "step_ms": step_stats(step_ms),
+            "l2": "256 MiB read-only L2 flush before every step (outside its CUDA events)",
+            "api": "StripStepper.step: one launch per step (round 1's headline protocol)"},
         "effective_gbs": achieved,
         "paper_model_gbs": paper_model_bytes(my_rows, cols, K) / mean_step / 1e9,
         "stage_updates_per_s": GV * (6 * K + 1) / mean_step,
@@ -563,14 +609,15 @@ def run_ours(args):
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": peak_src, "algorithmic_bytes_per_launch": bcomp,
                      "bytes_2d_per_launch": mpdata_2d_bytes(my_rows, cols),
-                     "per": "rank 0's fused launch(es) per step"},
+                     "per": "per step on rank 0: the persistent launch runs all K steps, so the "
+                            "kernel time per step = launch time / K (CUDA events on its stream)"},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "e2e_all_inputs": e2e_all,
         "e2e_time_loop": e2e_loop,
         "time_loop": loop,
         "o1280_strong": o1280,
-        "gpu_launches": args.steps * (1 if world == 1 or args.exchange == "p2p" else 3),
+        "gpu_launches": loop_launches,
         "clocks": clocks.summary(),
         "timed_wall_s": t_wall,
     }
@@ -582,7 +629,9 @@ def run_ours(args):
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[1])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--flushed-steps", type=int, default=50,
+                    help="steps of the step_flushed record (one launch each, L2 flushed before each)")
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--variant", type=int, default=0, help="fused tile variant (0 = default)")

@@ -226,6 +226,10 @@ int tsg_set_fused_schedule(int sched);
 /* Reads and clears the grid's dependency-wait error word: 2 when a persistent multi-step
  * launch timed out waiting for a neighbour tile (results of that launch are invalid). */
 int tsg_fused_wait_error(tsg_grid *g, int *err);
+/* Kernel launches tsg_mpdata_run (or tsg_mpdata_run_strip, on a strip grid) issues for
+ * `nsteps` steps under the current switches: 1 per 2^30 / units steps for the persistent
+ * loop, else one per step; -1 on error.  A benchmarking aid, no reference counterpart. */
+int tsg_fused_loop_launches(const tsg_grid *g, int nsteps);
 
 /* ---- neighbour reductions (stencil.py:401-408; kernels.py:27-104; reference.py:137-157) */
 /* Structured ("direct") reduce for any of the 9 relations (connectivity.py:36-68):

@@ -60,6 +60,7 @@ SIGNATURES = {
     "tsg_set_fused_band": (_c_int, [_c_int]),
     "tsg_set_fused_schedule": (_c_int, [_c_int]),
     "tsg_fused_wait_error": (_c_int, [_p, ctypes.POINTER(_c_int)]),
+    "tsg_fused_loop_launches": (_c_int, [_p, _c_int]),
     "tsg_time_loop_graphs_built": (_c_int, []),
     "tsg_launch_cache_stats": (_c_int, [_p, ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i64)]),
     "tsg_debug_trace": (_c_int, [_p]),

@@ -155,15 +155,22 @@ struct DynArgs {
     uint32_t whole;         // last step: tiles [0, whole) of the order dealt whole
     uint32_t items;         // items of the launch
     FastDiv fd_tiles, fd_chunks;
+    // MULTI + PEER (a row strip's persistent loop): the neighbours' halo rows written by the
+    // odd steps (FusedArgs::halo_up / _down: by the even steps), the per-step-parity count
+    // of finished boundary units, and how many units the boundary tile rows hold
+    double *halo_up_alt, *halo_down_alt;
+    int *bdone;
+    int nb_units;
 };
 
 // A tile shape of the dynamically dealt kernel: fn[kind][op], kind 0 = one step, 1 = one
-// row-strip step with the fused halo exchange (PEER), 2 = the persistent multi-step loop;
-// op 0 = upwind, 1 = centred, 2 = the data-movement probe (kind 0 only).
+// row-strip step with the fused halo exchange (PEER), 2 = the persistent multi-step loop,
+// 3 = the persistent loop of a row strip (multi-step + fused exchange); op 0 = upwind,
+// 1 = centred, 2 = the data-movement probe (kind 0 only).
 struct DynShape {
     int ti, tj, kc, stages, threads, smem;
     int multi_threads;  // the multi-step kernels add a signal warp
-    void *fn[3][3];
+    void *fn[4][3];
 };
 const DynShape *dyn_shape(int ti, int tj, int kc, int stages);
 

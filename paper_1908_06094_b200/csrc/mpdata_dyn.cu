@@ -87,6 +87,12 @@ __global__ void __launch_bounds__(TI *TJ * 8 + (MULTI ? 64 : 32), 1)
 
     const int tid = threadIdx.x;
     const int chunks = a.chunks;
+    // PEER: the global step this launch starts with (the device step counter, advanced by
+    // the previous launch; read before any CTA can finish this one)
+    int64_t wv = a.wait_value;
+    if constexpr (PEER) {
+        if (a.epoch) wv = *reinterpret_cast<volatile const int64_t *>(a.epoch);
+    }
     if (a.trace && tid == 0) a.trace[4 * blockIdx.x] = globaltimer_ns();
     if (tid == 0) {
         prefetch_tmap(&tm_pd);
@@ -120,6 +126,21 @@ __global__ void __launch_bounds__(TI *TJ * 8 + (MULTI ? 64 : 32), 1)
             if (inf.x < 0) break;
             mbar_wait(&dbar[stage], ph);
             mbar_arrive(&empty[stage]);
+            if constexpr (PEER) {
+                // a row strip's loop: the unit's stores into the neighbours' halo rows are
+                // made visible system-wide, and the last boundary unit of the step releases
+                // the step into both neighbours' flag words (what their boundary rows wait on)
+                if (inf.x == 0 || inf.x == a.tiles_i - 1) {
+                    __threadfence_system();
+                    if (atomicAdd(d.bdone + (inf.w & 1), 1) == d.nb_units - 1) {
+                        d.bdone[inf.w & 1] = 0;
+                        __threadfence_system();
+                        const int64_t v = wv + inf.w + 1;
+                        if (a.flag_up) asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(a.flag_up), "l"(v) : "memory");
+                        if (a.flag_down) asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(a.flag_down), "l"(v) : "memory");
+                    }
+                }
+            }
             if (inf.z == chunks - 1 && inf.w < d.nsteps - 1) {
                 const uint64_t f0 = a.trace ? globaltimer_ns() : 0;
                 red_release_gpu_add(d.tile_done + (int64_t)inf.x * a.tiles_j + inf.y, 1);
@@ -133,11 +154,8 @@ __global__ void __launch_bounds__(TI *TJ * 8 + (MULTI ? 64 : 32), 1)
     }
     if (tid >= kConsumers) {  // ---- the producer warp (one thread issues) ----
         if (tid != kConsumers) return;
-        int64_t wv = a.wait_value;  // PEER: the step this launch performs
-        if constexpr (PEER) {
-            if (a.epoch) wv = *reinterpret_cast<volatile const int64_t *>(a.epoch);
-        }
         bool waited = !(PEER && a.my_flags);
+        int waited_s = -1;  // MULTI + PEER: the last step whose neighbour flags were seen
         const uint64_t base = MULTI ? *reinterpret_cast<volatile const uint64_t *>(d.base) : 0;
         uint32_t n = 0;  // units issued
         uint32_t it = atomicAdd(&d.ticket[0], 1u);
@@ -153,7 +171,8 @@ __global__ void __launch_bounds__(TI *TJ * 8 + (MULTI ? 64 : 32), 1)
                 if (s > 0) {  // relaxed reads of the nine counters, checked after the slot wait
                     for (int q = 0; q < 9; ++q) {
                         int r = ti + q / 3 - 1, c = tj + q % 3 - 1;
-                        r = r < 0 ? r + a.tiles_i : (r >= a.tiles_i ? r - a.tiles_i : r);
+                        if (r < 0 || r >= a.tiles_i)  // a strip's row halo comes from the neighbours
+                            r = !(a.flags & TSG_PERIODIC_ROWS) ? ti : (r < 0 ? r + a.tiles_i : r - a.tiles_i);
                         c = c < 0 ? c + a.tiles_j : (c >= a.tiles_j ? c - a.tiles_j : c);
                         nbp[q] = d.tile_done + (int64_t)r * a.tiles_j + c;
                         nb[q] = ld_relaxed_gpu(nbp[q]);
@@ -188,7 +207,14 @@ __global__ void __launch_bounds__(TI *TJ * 8 + (MULTI ? 64 : 32), 1)
                         }
                     }
                     if constexpr (PEER) {
-                        if (!waited && (ti == 0 || ti == a.tiles_i - 1)) {  // reads the neighbours' rows
+                        // a boundary tile row reads the neighbours' rows of the previous step and
+                        // overwrites their halo rows read in it: wait for their step flags
+                        const bool boundary = ti == 0 || ti == a.tiles_i - 1;
+                        if (MULTI && a.my_flags && boundary && s > waited_s) {
+                            wait_both(a.my_flags, wv + s, a.timeout_ns, a.err);
+                            asm volatile("fence.proxy.async.global;" ::: "memory");
+                            waited_s = s;
+                        } else if (!MULTI && !waited && boundary) {
                             wait_both(a.my_flags, wv, a.timeout_ns, a.err);
                             asm volatile("fence.proxy.async.global;" ::: "memory");
                             waited = true;
@@ -221,6 +247,7 @@ __global__ void __launch_bounds__(TI *TJ * 8 + (MULTI ? 64 : 32), 1)
             d.ticket[0] = 0;
             d.ticket[1] = 0;
             if (MULTI) *d.base = base + (uint64_t)(d.nsteps - 1);  // one count per tile and step but the last
+            if (MULTI && PEER && a.epoch) *a.epoch = wv + d.nsteps;
         }
         return;
     }
@@ -240,6 +267,7 @@ __global__ void __launch_bounds__(TI *TJ * 8 + (MULTI ? 64 : 32), 1)
     int cur_ti = -1, cur_tj = -1, cur_par = -1;
     bool vvalid = false;
     int64_t cell = 0;
+    int vi = 0, vj = 0;  // this thread's vertex of the current tile
     VertexState vs{0, 0, 0, 0, 0, 0, 1.0, nullptr, nullptr, 0, 0};
     uint32_t n = 0;
     for (;; ++n) {
@@ -254,6 +282,8 @@ __global__ void __launch_bounds__(TI *TJ * 8 + (MULTI ? 64 : 32), 1)
             cur_tj = inf.y;
             cur_par = -1;
             const int i = a.row_lo + inf.x * TI + li, j = inf.y * TJ + lj;
+            vi = i;
+            vj = j;
             vvalid = i < a.row_hi && j < a.cols;
             if (vvalid) {
                 cell = (int64_t)(i + 1) * (a.cols + 2) + (j + 1);
@@ -267,11 +297,6 @@ __global__ void __launch_bounds__(TI *TJ * 8 + (MULTI ? 64 : 32), 1)
                 vs.dual = __ldg(a.dual + cell);
                 vs.d_row = 0;
                 vs.d_col = 0;
-                vs.peer = nullptr;
-                if constexpr (PEER) {
-                    if (i == 0 && a.halo_up) vs.peer = a.halo_up + (int64_t)(j + 1) * pv;
-                    else if (i == a.rows - 1 && a.halo_down) vs.peer = a.halo_down + (int64_t)(j + 1) * pv;
-                }
                 if (a.flags & TSG_PERIODIC_ROWS) {
                     if (i == 0) vs.d_row = (int64_t)a.rows * rowstride;
                     else if (i == a.rows - 1) vs.d_row = -(int64_t)a.rows * rowstride;
@@ -285,6 +310,12 @@ __global__ void __launch_bounds__(TI *TJ * 8 + (MULTI ? 64 : 32), 1)
         if (par != cur_par) {  // MULTI: odd steps write the other density buffer
             cur_par = par;
             vs.out = (par ? d.pd_alt : a.pd_out) + cell * pv;
+            vs.peer = nullptr;
+            if constexpr (PEER) {  // the neighbours' halo rows of that step's output buffer
+                double *hu = par ? d.halo_up_alt : a.halo_up, *hd = par ? d.halo_down_alt : a.halo_down;
+                if (vi == 0 && hu) vs.peer = hu + (int64_t)(vj + 1) * pv;
+                else if (vi == a.rows - 1 && hd) vs.peer = hd + (int64_t)(vj + 1) * pv;
+            }
         }
         mbar_wait(&full[stage], ph);
         if (!MULTI && a.trace && n == 0 && tid == 0) a.trace[4 * blockIdx.x + 1] = globaltimer_ns();
@@ -304,13 +335,12 @@ __global__ void __launch_bounds__(TI *TJ * 8 + (MULTI ? 64 : 32), 1)
         a.trace[4 * blockIdx.x + 2] = globaltimer_ns();
         if (!MULTI) a.trace[4 * blockIdx.x + 3] = (uint64_t)n;
     }
-    if constexpr (PEER) {
+    if constexpr (PEER && !MULTI) {
         asm volatile("bar.sync 1, %0;" ::"r"(kConsumers) : "memory");  // consumer warps only
         if (a.done && tid == 0) {  // the last CTA out releases the step into both neighbours
             __threadfence_system();
             if (atomicAdd(a.done, 1) == (int)gridDim.x - 1) {
                 *a.done = 0;
-                const int64_t wv = a.epoch ? *reinterpret_cast<volatile const int64_t *>(a.epoch) : a.wait_value;
                 if (a.epoch) *a.epoch = wv + 1;
                 __threadfence_system();
                 const int64_t v = wv + 1;
@@ -343,6 +373,9 @@ static DynShape make_shape() {
     v.fn[2][0] = (void *)mpdata_dyn_kernel<TI, TJ, KC, STAGES, TSG_UPWIND, false, true>;
     v.fn[2][1] = (void *)mpdata_dyn_kernel<TI, TJ, KC, STAGES, TSG_CENTRED, false, true>;
     v.fn[2][2] = nullptr;
+    v.fn[3][0] = (void *)mpdata_dyn_kernel<TI, TJ, KC, STAGES, TSG_UPWIND, true, true>;
+    v.fn[3][1] = (void *)mpdata_dyn_kernel<TI, TJ, KC, STAGES, TSG_CENTRED, true, true>;
+    v.fn[3][2] = nullptr;
     return v;
 }
 

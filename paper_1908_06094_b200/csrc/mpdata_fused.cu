@@ -567,8 +567,9 @@ struct FusedLaunch {
 // ---- device workspace of the dynamically dealt launches ----------------------------------
 // [0, 128): kLaunchCacheSize ticket slots of 4 words (one per cached launch, so launches
 // with different arguments never share a ticket); [128]: the tile counters' base (u64);
-// [136]: the dependency-wait error word; [256, ...): one u64 counter per tile.
-constexpr int kDynHeader = 256, kDynBaseOff = 128, kDynErrOff = 136;
+// [136]: the dependency-wait error word; [144]: two boundary-unit counters (a row strip's
+// persistent loop, self-resetting); [256, ...): one u64 counter per tile.
+constexpr int kDynHeader = 256, kDynBaseOff = 128, kDynErrOff = 136, kDynBdoneOff = 144;
 
 int tsg::create_dyn_workspace(tsg_grid *g) {
     // tile counters for the smallest dynamically dealt tile (4 x 12)
@@ -821,6 +822,7 @@ static int prepare_uncached(tsg_grid *g, const double *pd, const double *vn, con
         d.tile_done = reinterpret_cast<uint64_t *>(static_cast<unsigned char *>(g->dyn_ws) + kDynHeader);
         d.base = reinterpret_cast<uint64_t *>(static_cast<unsigned char *>(g->dyn_ws) + kDynBaseOff);
         d.err = reinterpret_cast<int *>(static_cast<unsigned char *>(g->dyn_ws) + kDynErrOff);
+        d.bdone = reinterpret_cast<int *>(static_cast<unsigned char *>(g->dyn_ws) + kDynBdoneOff);
         d.timeout_ns = 20ull * 1000000000ull;
         d.pd_alt = nullptr;
         if (int rc = set_smem_once(L->fn, ds->smem)) return rc;
@@ -1101,6 +1103,43 @@ extern "C" int tsg_mpdata_run_strip(tsg_grid *g, double *pd_a, double *pd_b, con
                                halo_down_a, my_flags, flag_up, flag_down, 0, epoch, timeout_ms,
                                error_word, done_counter, &fwd))
         return rc;
+    if (fwd.dyn) {  // the whole loop in persistent launches: per-step exchange inside the kernel
+        int n = 0;
+        const Variant &v = variants(&n)[pick_variant(g, g->rows) - 1];
+        const DynShape *ds = dyn_shape(v.ti, v.tj, v.kc, v.stages);
+        if (ds && (int64_t)fwd.a.tiles_i * fwd.a.tiles_j <= g->dyn_tiles) {
+            FusedLaunch M = fwd;
+            M.fn = ds->fn[3][flux_op];
+            M.coop = true;
+            M.threads = ds->multi_threads;
+            if (int rc = set_smem_once(M.fn, ds->smem)) return rc;
+            if (int rc = encode_pd(v, g, pd_b, &M.m_pd_alt)) return rc;
+            M.d.pd_alt = pd_a;
+            M.d.halo_up_alt = halo_up_b;
+            M.d.halo_down_alt = halo_down_b;
+            M.d.nb_units = (fwd.a.tiles_i > 1 ? 2 : 1) * fwd.a.tiles_j * fwd.a.chunks;
+            const int64_t T = (int64_t)fwd.a.tiles_i * fwd.a.tiles_j;
+            int64_t smax = ((int64_t)1 << 30) / (T * fwd.a.chunks);
+            smax = smax < 2 ? 2 : (smax & ~(int64_t)1);
+            bool ab = true;
+            for (int left = nsteps; left > 0;) {
+                const int S = (int)(left < smax ? left : smax);
+                FusedLaunch X = M;
+                if (!ab) {
+                    std::swap(X.m_pd, X.m_pd_alt);
+                    X.a.pd_out = pd_a;
+                    X.d.pd_alt = pd_b;
+                    std::swap(X.a.halo_up, X.d.halo_up_alt);
+                    std::swap(X.a.halo_down, X.d.halo_down_alt);
+                }
+                set_dyn_items(&X, S);
+                if (int rc = launch(&X, s)) return rc;
+                if (S % 2) ab = !ab;
+                left -= S;
+            }
+            return TSG_OK;
+        }
+    }
     if (int rc = prepare_strip(g, pd_b, vn, wn, rho, signs, dual, pd_a, dt, pivbz, flux_op, halo_up_b,
                                halo_down_b, my_flags, flag_up, flag_down, 0, epoch, timeout_ms,
                                error_word, done_counter, &bwd))
@@ -1118,6 +1157,28 @@ extern "C" int tsg_time_loop_graphs_built(void) { return g_graph_builds; }
 extern "C" int tsg_debug_trace(uint64_t *per_cta4) {
     g_trace = per_cta4;  // NULL switches the trace off
     return TSG_OK;
+}
+
+// Kernel launches tsg_mpdata_run / _run_strip issue for `nsteps` steps on this grid under
+// the current switches (the benchmark's launch count), or -1.
+extern "C" int tsg_fused_loop_launches(const tsg_grid *g, int nsteps) {
+    if (!g || nsteps < 0) {
+        fail(TSG_EVALUE, "grid is NULL or nsteps < 0");
+        return -1;
+    }
+    if (nsteps == 0) return 0;
+    int n = 0;
+    const Variant &v = variants(&n)[pick_variant(g, g->rows) - 1];
+    const int tiles_i = (g->rows + v.ti - 1) / v.ti, tiles_j = (g->cols + v.tj - 1) / v.tj;
+    const int chunks = (g->levels + v.kc - 1) / v.kc;
+    const bool strip = !(g->flags & TSG_PERIODIC_ROWS);
+    if (g_sched == 0 && v.dyn_ok && g->dyn_ws && (int64_t)tiles_i * tiles_j <= g->dyn_tiles &&
+        (strip || nsteps >= 2)) {
+        int64_t smax = ((int64_t)1 << 30) / ((int64_t)tiles_i * tiles_j * chunks);
+        smax = smax < 2 ? 2 : (smax & ~(int64_t)1);
+        return (int)((nsteps + smax - 1) / smax);
+    }
+    return nsteps;
 }
 
 extern "C" int tsg_fused_wait_error(tsg_grid *g, int *err) {

@@ -378,14 +378,24 @@ class StripStepper:
                   ctypes.c_void_p(down["flags"].ptr), n + 1, s)
 
     def run(self, steps: int, dt: float, pivbz: float) -> None:
-        """``steps`` x (step; swap).  With the one-launch p2p exchange the loop is a captured
-        two-step CUDA graph (tsg_mpdata_run_strip): halo stores, fences and the step counter
-        all on the device, one graph launch per two steps."""
+        """``steps`` x (step; swap).  One GPU: tsg_mpdata_run (the persistent multi-step
+        kernel).  With the one-launch p2p exchange: tsg_mpdata_run_strip -- the persistent
+        loop of a row strip (halo-row stores, per-step neighbour flags and the step counter
+        all inside the kernel), or with the static schedule a captured two-step graph."""
         import ctypes
 
         steps = int(steps)
         if steps < 0:
             raise ValueError(f"steps must be >= 0, got {steps}")
+        if self.world == 1 and steps:  # the periodic patch: tsg_mpdata_run (persistent loop)
+            _lib.call("tsg_mpdata_run", self.grid.handle, _lib.ptr(self.pd), _lib.ptr(self.pd_out),
+                      _lib.ptr(self.vn), _lib.ptr(self.wn), _lib.ptr(self.rho), _lib.ptr(self.signs),
+                      _lib.ptr(self.dual), float(dt), float(pivbz), self.flux_code, steps,
+                      _lib.stream_handle())
+            self.steps_done += steps
+            if steps % 2:  # the newest density landed in pd_out
+                self.pd, self.pd_out = self.pd_out, self.pd
+            return
         if self.mode != "p2p" or not self.single_launch or steps == 0:
             for _ in range(steps):
                 self.step(dt, pivbz)

@@ -216,7 +216,12 @@ def _p2p_worker(rank, world, port, q, single_launch=True, graph=False, shape=(17
         rows, cols, K = shape
         st = StripStepper(rows, cols, K, rank, world, seed=7, mode="p2p", timeout_ms=60000,
                           single_launch=single_launch)
-        if graph:  # 1 + 5 steps: the captured two-step graph, an odd tail, a rebuilt graph
+        if graph == "mixed":  # persistent loops and single-launch steps share the step counter
+            st.run(2, 0.2, 0.8)
+            st.step(0.2, 0.8)
+            st.swap()
+            st.run(3, 0.2, 0.8)
+        elif graph:  # 1 + 5 steps: persistent loop launches (or the captured graph), odd tail
             st.run(1, 0.2, 0.8)
             st.run(5, 0.2, 0.8)
         else:
@@ -246,7 +251,8 @@ def _p2p_worker(rank, world, port, q, single_launch=True, graph=False, shape=(17
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,single_launch,graph,shape", [
     (2, True, False, (17, 29, 18)), (2, False, False, (17, 29, 18)), (3, True, False, (17, 29, 18)),
-    (2, True, True, (17, 29, 18)),
+    (2, True, True, (17, 29, 18)), (3, True, True, (17, 29, 18)), (2, True, "mixed", (17, 29, 18)),
+    (2, True, True, (9, 40, 80)),
     # strips large enough for the band schedule (interior rows banded, boundary rows last)
     (2, True, True, (512, 608, 32))])
 def test_p2p_fused_exchange_processes_share_one_gpu(cuda_ok, world, single_launch, graph, shape):

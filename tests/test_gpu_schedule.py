@@ -121,3 +121,18 @@ def test_dynamic_deal_balances_the_ctas(cuda_ok):
     units = t[:, 3]
     assert units.sum() == 70 * 16 * 5  # tiles x chunks of the 4x16x16 unit
     assert units.min() >= 1
+
+
+def test_strip_stepper_run_on_one_gpu_is_the_persistent_loop(cuda_ok):
+    """StripStepper(world=1).run(n) (tsg_mpdata_run) == n x (step; swap), both parities."""
+    from paper_1908_06094_b200.distributed import StripStepper
+
+    for n in (4, 5):
+        a = StripStepper(31, 48, 33, 0, 1, seed=2)
+        b = StripStepper(31, 48, 33, 0, 1, seed=2)
+        a.run(n, 0.2, 0.8)
+        for _ in range(n):
+            b.step(0.2, 0.8)
+            b.swap()
+        assert np.array_equal(a.interior("pd").cpu().numpy(), b.interior("pd").cpu().numpy())
+        assert a.steps_done == b.steps_done == n

@@ -1,12 +1,3 @@
-nvidia-smi --query-gpu=timestamp,clocks.sm,power.draw,clocks_event_reasons.active,temperature.gpu --format=csv -lms 100 > gpurun_out/clk.csv &
-SMI=$!
-timeout 300 python tools/time_loop.py --sched 0 --n 100,1000,1000,100,10
-timeout 300 python tools/time_loop.py --sched 1 --n 100,1000,1000,100,10
-kill $SMI
-python - <<'PY'
-import csv
-rows=list(csv.reader(open('gpurun_out/clk.csv')))[1:]
-import collections
-print(len(rows))
-for r in rows[::10]: print(",".join(x.strip() for x in r))
-PY
+timeout 300 python tools/e2e_ab.py
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:mpdata_dyn -s 1 -c 1 -o gpurun_out/prof_loop_r2d -f python tools/prof_loop.py 10 > gpurun_out/ncu_loop_r2d.log 2>&1; tail -2 gpurun_out/ncu_loop_r2d.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:mpdata_dyn -s 2 -c 1 -o gpurun_out/prof_step_r2d -f python tools/prof_fused.py 0 4 > gpurun_out/ncu_step_r2d.log 2>&1; tail -2 gpurun_out/ncu_step_r2d.log
