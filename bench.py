@@ -300,6 +300,21 @@ def _timed_steps(stepper, steps, stream, flush_l2=None):
     return [a.elapsed_time(b) for a, b in evs]
 
 
+def _timed_run(stepper, steps, stream) -> float:
+    """Device time (s) of ``stepper.run(steps)`` -- one persistent launch -- between CUDA
+    events on ``stream``; a device sleep queued first keeps the host's launch preparation
+    off the measured interval (the GPU is busy until the launch is queued)."""
+    import torch
+
+    torch.cuda._sleep(SLEEP_CYCLES)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    stepper.run(steps, DT, PIVBZ)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3
+
+
 def _max_over_ranks(x: float, world: int, shared: bool) -> float:
     if world == 1:
         return x
@@ -326,17 +341,12 @@ def o1280_strong(args, rank, world, shared, barrier, peak):
     if world > 1:
         st.check()
     barrier()
-    stream = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    st.run(args.o1280_steps, DT, PIVBZ)  # the dependent loop, as the headline
-    e1.record(stream)
-    torch.cuda.synchronize()
+    t_run = _timed_run(st, args.o1280_steps, torch.cuda.current_stream())  # the dependent loop
     barrier()
     if world > 1:
         st.finish()
         st.check()
-    t = _max_over_ranks(e0.elapsed_time(e1) / 1e3, world, shared) / args.o1280_steps
+    t = _max_over_ranks(t_run, world, shared) / args.o1280_steps
     mine = mpdata_algorithmic_bytes(st.nrows, C, K)
     rec = {"value": R * C * K / t, "unit": UNIT, "n_gpus": world, "scaling": "strong",
            "ms_per_step": t * 1e3, "steps": args.o1280_steps,
@@ -454,17 +464,13 @@ def run_ours(args):
         torch.cuda.synchronize()
         barrier()
         t_wall0 = time.perf_counter()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        stepper.run(args.steps, DT, PIVBZ)  # the timed region: K dependent steps
-        ev1.record(stream)
-        torch.cuda.synchronize()
+        t_run = _timed_run(stepper, args.steps, stream)  # the timed region: K dependent steps
         barrier()
         t_wall = time.perf_counter() - t_wall0
         if world > 1:
             stepper.finish()
             stepper.check()
-        total_s = _max_over_ranks(ev0.elapsed_time(ev1) / 1e3, world, shared)
+        total_s = _max_over_ranks(t_run, world, shared)
         mean_step = total_s / args.steps
         value = GV * K / mean_step
         loop_launches = (_lib.lib().tsg_fused_loop_launches(stepper.grid.handle, args.steps)
@@ -532,14 +538,9 @@ def run_ours(args):
                 st.run(n_loop, DT, PIVBZ)
                 flush_l2()
                 torch.cuda.synchronize()
-                l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                l0.record(stream)
-                st.run(n_loop, DT, PIVBZ)
-                l1.record(stream)
-                torch.cuda.synchronize()
+                t_loop = _timed_run(st, n_loop, stream) / n_loop
             finally:
                 _lib.call("tsg_set_fused_schedule", 0)
-            t_loop = l0.elapsed_time(l1) / 1e3 / n_loop
             loop = {"value": V * K / t_loop, "unit": UNIT, "ms_per_step": t_loop * 1e3, "steps": n_loop,
                     "roofline_frac": mpdata_algorithmic_bytes(w["rows"], cols, K) / t_loop / 1e9 / peak,
                     "api": "StructuredStepper.run with tsg_set_fused_schedule(1): static per-CTA ranges, "
@@ -561,8 +562,8 @@ def run_ours(args):
     traffic, traffic_src = None, None
     tfile = ROOT / "profiles" / "fused_traffic.json"
     if tfile.exists() and world == 1 and args.workload == "cfg3":
-        tj = json.loads(tfile.read_text())  # the ncu capture of the 279x256x80 launch
-        traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("source")
+        tj = json.loads(tfile.read_text())  # the ncu capture of the 279x256x80 loop kernel
+        traffic, traffic_src = tj.get("dram_bytes_per_step"), tj.get("source")
     import ctypes
 
     vi = [ctypes.c_int() for _ in range(6)]

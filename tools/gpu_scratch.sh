@@ -1,3 +1,1 @@
-timeout 300 python tools/e2e_ab.py
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:mpdata_dyn -s 1 -c 1 -o gpurun_out/prof_loop_r2d -f python tools/prof_loop.py 10 > gpurun_out/ncu_loop_r2d.log 2>&1; tail -2 gpurun_out/ncu_loop_r2d.log
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:mpdata_dyn -s 2 -c 1 -o gpurun_out/prof_step_r2d -f python tools/prof_fused.py 0 4 > gpurun_out/ncu_step_r2d.log 2>&1; tail -2 gpurun_out/ncu_step_r2d.log
+for w in 2 3 4; do timeout 1500 python tools/o1280_strips_check.py 3 $w 2>&1 | tail -2; done | tee gpurun_out/o1280_strips_r2.log

@@ -1,6 +1,7 @@
 """cfg5 parity at full size: the O1280-class patch (2560x2576x137) stepped as
-two row strips in two processes sharing one GPU (fused P2P exchange, one launch per step,
-graph-captured loop) against the single-patch step, compared bitwise through a device-side
+two (or more) row strips in as many processes sharing one GPU (the persistent strip loop:
+fused P2P exchange, per-step neighbour flags inside one launch) against the single-patch
+persistent loop and the static per-step schedule, compared bitwise through a device-side
 hash of every interior row.  Needs ~110 GB of device memory; not part of the test suite.
 
     python tools/o1280_strips_check.py [steps] [strips]
@@ -41,12 +42,20 @@ def worker(rank, world, port, steps, q):
     parts = [None] * world
     dist.all_gather_object(parts, mine)
     if rank == 0:
-        single = StripStepper(ROWS, COLS, K, 0, 1, seed=11)
-        single.run(steps, 0.05, 0.9)
-        torch.cuda.synchronize()
-        want = row_hashes(single.interior("pd")[..., :K]).cpu()
+        from paper_1908_06094_b200 import _lib
+
         got = torch.cat([h for _, h in sorted(parts, key=lambda p: p[0])])
-        q.put(bool(torch.equal(got, want)))
+        res = {}
+        for sched in (0, 1):  # the persistent loop, and the static per-step schedule
+            _lib.call("tsg_set_fused_schedule", sched)
+            single = StripStepper(ROWS, COLS, K, 0, 1, seed=11)
+            single.run(steps, 0.05, 0.9)
+            torch.cuda.synchronize()
+            res[sched] = row_hashes(single.interior("pd")[..., :K]).cpu()
+            del single
+            torch.cuda.empty_cache()
+        _lib.call("tsg_set_fused_schedule", 0)
+        q.put((bool(torch.equal(got, res[0])), bool(torch.equal(res[0], res[1])), int(got.numel())))
     dist.destroy_process_group()
 
 
@@ -62,8 +71,10 @@ if __name__ == "__main__":
     ps = [ctx.Process(target=worker, args=(r, world, port, steps, q)) for r in range(world)]
     for p in ps:
         p.start()
-    ok = q.get(timeout=3000)
+    ok, ok_static, nrows = q.get(timeout=3000)
     for p in ps:
         p.join()
-    print(f"O1280 {ROWS}x{COLS}x{K}, {world} strips vs single patch, {steps} steps: "
-          f"bitwise {'EQUAL' if ok else 'DIFFERENT'}")
+    print(f"O1280 {ROWS}x{COLS}x{K}, {world} strips (persistent strip loops, fused P2P exchange) vs "
+          f"the single patch (persistent loop), {steps} steps, {nrows} row hashes: "
+          f"bitwise {'EQUAL' if ok else 'DIFFERENT'}; single patch persistent loop vs static "
+          f"per-step schedule: {'EQUAL' if ok_static else 'DIFFERENT'}", flush=True)
