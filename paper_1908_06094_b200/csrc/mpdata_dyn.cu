@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(TI *TJ * 8 + (MULTI ? 64 : 32), 1)
         prefetch_tmap(&tm_rho);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], MULTI ? 1 : kWarps);  // MULTI: the signal warp releases
+            mbar_init(&empty[s], kWarps + (MULTI ? 1 : 0));  // MULTI: the signal warp too
             mbar_init(&ibar[s], 1);
             if (MULTI) mbar_init(&dbar[s], kWarps);
         }
@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(TI *TJ * 8 + (MULTI ? 64 : 32), 1)
     if (MULTI && tid >= kConsumers + 32) {  // ---- the signal warp (MULTI) ----
         // Publishes finished tiles for the other CTAs' dependency waits, off the consumers'
         // and the producer's paths: per unit it waits until every consumer warp is done
-        // (dbar), releases the stage to the producer (empty), and after a tile's last chunk
+        // (dbar), releases the stage to the producer (its arrival completes `empty` with the
+        // consumer warps' own), and after a tile's last chunk
         // adds 1 to the tile's counter with gpu-scope release semantics -- cumulative over
         // the consumer warps' pd_out stores it acquired through the mbarrier.  It never lags
         // more than one phase: the producer cannot refill a stage it has not released.
@@ -329,7 +330,10 @@ __global__ void __launch_bounds__(TI *TJ * 8 + (MULTI ? 64 : 32), 1)
                                                 a.K, a.dt, a.pivbz);
         }
         __syncwarp();
-        if ((tid & 31) == 0) mbar_arrive(MULTI ? &dbar[stage] : &empty[stage]);
+        if ((tid & 31) == 0) {
+            if (MULTI) mbar_arrive(&dbar[stage]);  // for the signal warp
+            mbar_arrive(&empty[stage]);
+        }
     }
     if (a.trace && tid == 0) {
         a.trace[4 * blockIdx.x + 2] = globaltimer_ns();

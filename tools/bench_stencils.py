@@ -27,7 +27,8 @@ from paper_1908_06094_b200 import (LocationType as L, Numbering, OFFSET_TABLES, 
                                    build_neighbor_table, element_count, make_permutation)
 from paper_1908_06094_b200.device import DeviceGrid  # noqa: E402
 
-PEAK = 6537.6
+_pk = Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"
+PEAK = json.loads(_pk.read_text())["hbm_gbs"] if _pk.exists() else 6650.0  # fallback (B200_PROFILING.md)
 flush = torch.ones(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
 sink = torch.empty(1, dtype=torch.float64, device="cuda")
 OUT = []
@@ -160,11 +161,20 @@ def fusion(rows, cols, K):
     record("mpdata_indirect", t3, unfused_bytes + 8 * v * K, patch=[rows, cols, K], updates_per_s=v * K / t3)
 
 
+def launch_floor():
+    """The protocol's fixed cost: an empty launch between the same CUDA events after the
+    same L2 flush (no kernel at all: just the events' own interval)."""
+    record("launch_floor_empty_kernel", timed(lambda: torch.cuda._sleep(1)), 0)
+    record("launch_floor_no_kernel", timed(lambda: None), 0)
+
+
 if __name__ == "__main__":
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    launch_floor()
     table1(128, 128, 80)
     table1(1024, 1024, 80)
     relations(256, 256, 80)
+    relations(1024, 1024, 80)
     cell_div(256, 256, 80)
     fusion(279, 256, 80)
     fusion(2560, 2576, 137)

@@ -1,1 +1,2 @@
-for w in 2 3 4; do timeout 1500 python tools/o1280_strips_check.py 3 $w 2>&1 | tail -2; done | tee gpurun_out/o1280_strips_r2.log
+CS=/usr/local/cuda/bin/compute-sanitizer
+timeout 900 $CS --tool racecheck --print-limit 5 python tools/sanitize_dyn.py 64x128x32 > gpurun_out/san_rc2.log 2>&1; grep -v "^=========     \(#\|in \|Saved\)" gpurun_out/san_rc2.log | tail -5
