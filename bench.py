@@ -223,19 +223,29 @@ def reference_python_record(w: dict, reps: int) -> dict | None:
                       f"(its fastest path), median of {reps} via its time_computation"}
 
 
+def cpu_baseline(args, w: dict) -> dict:
+    """The one CPU-baseline protocol both arms use: the C port on every host core,
+    ``--warmup`` untimed steps, then ``--steps`` timed ones (3 for the O1280 sample) capped
+    at ``--cpu-seconds``, median; run before any CUDA work in the process."""
+    steps = args.steps if args.workload == "cfg3" else min(args.steps, 3)
+    times, threads = cpu_port_sample(w["cpu_rows"], w["cols"], w["levels"], args.warmup, steps=steps,
+                                     budget_s=args.cpu_seconds)
+    rec = cpu_record(w, times, threads)
+    rec["steps"] = len(times)
+    return rec
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     w = WORKLOADS[args.workload]
-    steps = args.steps if args.workload == "cfg3" else min(args.steps, 3)
-    times, threads = cpu_port_sample(w["cpu_rows"], w["cols"], w["levels"], args.warmup, steps=steps)
-    cpu = cpu_record(w, times, threads)
+    cpu = cpu_baseline(args, w)
     value = cpu["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": len(times), "warmup": args.warmup, "ms_per_step": cpu["ms_per_step"],
+        "steps": cpu["steps"], "warmup": args.warmup, "ms_per_step": cpu["ms_per_step"],
         "higher_is_better": True, "scaling": w["scaling"], "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": workload_config(w, world),
@@ -415,6 +425,9 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # the host baseline (N = 1 only), first, so it sees the same process state as the
+    # reference arm's identical sample
+    cpu = cpu_baseline(args, WORKLOADS[args.workload]) if not args.no_cpu and world == 1 else None
     # TSG_SHARE_ONE_GPU=1: every rank on cuda:0 with gloo -- exercises the N>1 code path on
     # a one-GPU box (not a performance configuration)
     shared = os.environ.get("TSG_SHARE_ONE_GPU") == "1"
@@ -568,10 +581,6 @@ def run_ours(args):
 
     vi = [ctypes.c_int() for _ in range(6)]
     _lib.lib().tsg_fused_variant_info(variant, *[ctypes.byref(x) for x in vi])
-    cpu = None
-    if not args.no_cpu and world == 1:  # the host baseline is measured at N = 1 only
-        times, threads = cpu_port_sample(w["cpu_rows"], cols, K, args.warmup, budget_s=args.cpu_seconds)
-        cpu = cpu_record(w, times, threads)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": mean_step * 1e3, "higher_is_better": True,

@@ -206,6 +206,10 @@ int tsg_transport_indirect(const int64_t *e2v, const int64_t *v2e, const double 
  * forced variant, or the compact tile when none is forced; `threads` counts the producer
  * warp. */
 int tsg_set_fused_variant(int variant);
+/* Benchmarking hook: force an alternative compact tile shape of the TMA neighbour reduce's
+ * plain sum fold (1-9 static ranges, 11-19 the same shapes dynamically dealt); 0 (the
+ * default) = the measured per-source-location shape and schedule. */
+int tsg_set_reduce_variant(int variant);
 int tsg_fused_variant_info(int variant, int *ti, int *tj, int *kc, int *stages, int *threads,
                            int *smem_bytes);
 /* The variant a fused launch over logical rows [row_lo, row_hi) of `g` uses (-1 on error). */

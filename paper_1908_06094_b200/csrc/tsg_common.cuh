@@ -24,6 +24,9 @@ struct tsg_grid {
 };
 
 namespace tsg {
+// dyn_ws header bytes [192, 200): the dynamically dealt TMA reduce's ticket words
+// (reduce_tma.cu); [0, 160) belong to the fused launches (mpdata_fused.cu)
+constexpr int kDynReduceTicketOff = 192;
 void destroy_graph_cache(tsg_grid *g);
 void destroy_launch_cache(tsg_grid *g);
 int create_dyn_workspace(tsg_grid *g);

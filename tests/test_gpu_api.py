@@ -592,3 +592,53 @@ def test_tma_reduce_and_cell_divergence_paths(cuda_ok, shape):
         out = T.make_storage(spec, L.CELLS, "div_out")
         T.run_gpu(T.build_divergence(spec, state, geo, weighted=weighted, out=out))
         assert np.array_equal(T.field_to_flat(out), want), weighted
+
+
+def test_tma_reduce_dynamic_deal_matches_oracle(cuda_ok):
+    """A patch with >= 24 units per resident CTA takes the dynamically dealt reduce
+    (reduce_tma.cu kRedDynUnits): all nine relations, the scaled Table-1 kernel and the
+    cell divergence against the oracle, bitwise; twice, so the ticket reset is exercised."""
+    r, c, lev = 512, 512, 33
+    spec = T.PatchSpec(r, c, lev)
+    rng = np.random.default_rng(5)
+    for (f, t) in T.OFFSET_TABLES:
+        src = T.make_storage(spec, t, "a")
+        dst = T.make_storage(spec, f, "b")
+        a = rng.random((T.element_count(spec, t), lev))
+        T.flat_to_field(a, src)
+        want = O.neighbor_sum(O.neighbor_table(r, c, f.value, t.value), a)
+        for _ in range(2):
+            T.run_gpu(T.build_reduce(spec, f, t, src, dst))
+            assert np.array_equal(T.field_to_flat(dst), want), (f, t)
+    fields = T.make_kernel_fields(spec)
+    a = rng.random((2 * r * c, lev))
+    fac = 0.5 + rng.random((2 * r * c, 1))
+    T.flat_to_field(a, fields["a"])
+    T.flat_to_field(fac, fields["fac"])
+    T.run_gpu(T.build_kernel(spec, fields, True))
+    want = O.neighbor_sum_scaled(O.neighbor_table(r, c, "cells", "cells"), a, fac)
+    assert np.array_equal(T.field_to_flat(fields["b"]), want)
+
+
+def test_tma_reduce_every_tile_shape(cuda_ok):
+    """Every benchmarking shape of the TMA reduce (tsg_set_reduce_variant: static 1-9,
+    dynamically dealt 11-19) is bitwise equal to the oracle on a ragged patch with an odd
+    level count."""
+    from paper_1908_06094_b200 import _lib
+
+    r, c, lev = 37, 70, 35
+    spec = T.PatchSpec(r, c, lev)
+    rng = np.random.default_rng(11)
+    try:
+        for (f, t) in T.OFFSET_TABLES:
+            src = T.make_storage(spec, t, "a")
+            dst = T.make_storage(spec, f, "b")
+            a = rng.random((T.element_count(spec, t), lev))
+            T.flat_to_field(a, src)
+            want = O.neighbor_sum(O.neighbor_table(r, c, f.value, t.value), a)
+            for v in list(range(0, 10)) + list(range(11, 20)):
+                _lib.call("tsg_set_reduce_variant", v)
+                T.run_gpu(T.build_reduce(spec, f, t, src, dst))
+                assert np.array_equal(T.field_to_flat(dst), want), (f, t, v)
+    finally:
+        _lib.call("tsg_set_reduce_variant", 0)

@@ -34,13 +34,17 @@ sink = torch.empty(1, dtype=torch.float64, device="cuda")
 OUT = []
 
 
-def timed(fn, reps=30, warm=3):
+def timed(fn, reps=100, warm=3):
+    """Mean device time of ``fn`` over ``reps`` launches, each after an L2 flush and a ~50 us
+    device sleep (so the launch is queued before the GPU reaches it: no host preparation
+    inside the events).  The mean, because event timestamps tick every ~2 us here."""
     for _ in range(warm):
         fn()
     ev = []
     for _ in range(reps):
         sink.copy_(flush.sum().reshape(1))
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(100_000)
         a.record()
         fn()
         b.record()
@@ -176,6 +180,7 @@ if __name__ == "__main__":
     relations(256, 256, 80)
     relations(1024, 1024, 80)
     cell_div(256, 256, 80)
+    cell_div(1024, 1024, 80)
     fusion(279, 256, 80)
     fusion(2560, 2576, 137)
     Path("gpurun_out").mkdir(exist_ok=True)

@@ -1,6 +1,9 @@
+# Round-end rehearsal on one GPU: the driver's GPU tiers (pytest -m gpu, smoke, both bench
+# arms, a 2-rank bench sharing the GPU).  Logs land in gpurun_out/.
 set -x
+mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -25 > gpurun_out/gputest.log
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -25 > gpurun_out/gputest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1
