@@ -336,6 +336,17 @@ def _max_over_ranks(x: float, world: int, shared: bool) -> float:
     return float(t.item())
 
 
+def _sm_clock_mhz(index: int):
+    """The SM clock now (NVML), or None."""
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        return pynvml.nvmlDeviceGetClockInfo(pynvml.nvmlDeviceGetHandleByIndex(index), pynvml.NVML_CLOCK_SM)
+    except Exception:  # informational only
+        return None
+
+
 def o1280_strong(args, rank, world, shared, barrier, peak):
     """configs[4] strong scaling: the O1280-class patch in `world` strips, same path."""
     import torch
@@ -357,6 +368,19 @@ def o1280_strong(args, rank, world, shared, barrier, peak):
         st.finish()
         st.check()
     t = _max_over_ranks(t_run, world, shared) / args.o1280_steps
+    sm_after = _sm_clock_mhz(0 if shared else torch.cuda.current_device())
+    # the same step isolated: 200 ms idle before each (the SM clock back at its boost
+    # value), so the power-capped sustained loop above can be read against it
+    iso = []
+    for _ in range(3):
+        time.sleep(0.2)
+        barrier()
+        iso.append(_timed_run(st, 1, torch.cuda.current_stream()))
+    barrier()
+    if world > 1:
+        st.finish()
+        st.check()
+    t_iso = _max_over_ranks(statistics.median(iso), world, shared)
     mine = mpdata_algorithmic_bytes(st.nrows, C, K)
     rec = {"value": R * C * K / t, "unit": UNIT, "n_gpus": world, "scaling": "strong",
            "ms_per_step": t * 1e3, "steps": args.o1280_steps,
@@ -365,7 +389,11 @@ def o1280_strong(args, rank, world, shared, barrier, peak):
            "path": f"StripStepper ({'periodic patch' if world == 1 else st.mode + ' exchange'})",
            "inputs": "on-device counter hash of global ids (identical for every N)",
            "l2": "no flush: per-GPU state >= 6.3 GB",
-           "efficiency": "T1 / (N * T_N) with T1 = the N = 1 run's o1280_strong.ms_per_step"}
+           "efficiency": "T1 / (N * T_N) with T1 = the N = 1 run's o1280_strong.ms_per_step",
+           "sm_mhz_after_loop": sm_after,
+           "isolated_step": {"ms_per_step": t_iso * 1e3, "roofline_frac": mine / t_iso / 1e9 / peak,
+                             "how": "one step after 200 ms idle, median of 3 (SM clock at boost; the "
+                                    "loop above runs long enough to reach the power cap)"}}
     del st
     torch.cuda.empty_cache()
     return rec

@@ -57,8 +57,12 @@ inline int colors_of(int loc) { return loc == TSG_VERTICES ? 1 : (loc == TSG_CEL
 // multiple of 16, so every element's level run starts on a 128-byte line and a 16-level
 // TMA chunk is whole lines (O1280, K = 137: 10.3 vs 10.6 ms per fused step), at <= 19 %
 // padding that the tensor maps never fetch (their level extent is the logical count).
+#ifndef TSG_LONG_PITCH_ALIGN  // A/B builds only (-DTSG_LONG_PITCH_ALIGN=2)
+#define TSG_LONG_PITCH_ALIGN 16
+#endif
 __host__ __device__ inline int64_t pitch_of(int inner) {
-    return inner <= 1 ? 1 : (inner < 64 ? ((inner + 1) & ~1) : ((inner + 15) & ~15));
+    constexpr int kA = TSG_LONG_PITCH_ALIGN;
+    return inner <= 1 ? 1 : (inner < 64 ? ((inner + 1) & ~1) : ((inner + kA - 1) / kA * kA));
 }
 inline bool valid_loc(int loc) { return loc >= 0 && loc <= 2; }
 

@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-timeout 900 python tools/bench_stencils.py r2 > gpurun_out/stencils_r2.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_table1_small_r2.csv python tools/prof_table1_small.py > /dev/null 2>&1
-tail -3 gpurun_out/stencils_r2.log
+timeout 600 python tools/e2e_loop_breakdown.py 20 > gpurun_out/e2e_breakdown.log 2>&1
+cat gpurun_out/e2e_breakdown.log
+nproc; lscpu | grep -i "model name\|socket\|numa node(s)"
