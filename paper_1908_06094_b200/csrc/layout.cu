@@ -81,27 +81,50 @@ __global__ void __launch_bounds__(256) unpack_lines_kernel(FieldIx F, int inner,
 // idle in the second pass of an 80-level run and are latency-bound).
 constexpr int kItemUnroll = 4;
 
+// The gathered side of pack is a dependent load (forward[e], then the flat row), so the
+// next batch's element ids and ranks are fetched while this batch's rows are in flight:
+// one load latency per batch instead of two (the unpack side stores through the rank and
+// does not wait on it).  One item per batch: the fewest registers, so the most resident
+// threads -- 1024x1024x80 SN / UN / HN 433 / 450 / 448 us (0.93-0.96 of the copy peak)
+// against 445-470 us with two items, 520-540 with three and 529-548 us for round 1's
+// unpipelined four (tools/pack_variants.py, TSG_PACK_V A/B build).
+constexpr int kPackUnroll = 1;
+template <int U>
 __global__ void __launch_bounds__(256) pack_pairs_kernel(FieldIx F, int inner, PointDec D,
                                                          const double *__restrict__ flat,
                                                          const int64_t *__restrict__ forward,
                                                          double *__restrict__ f, int flags) {
+    constexpr int kItemUnroll = U;
     const uint32_t T = gridDim.x * blockDim.x;
-    for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < D.n; base += kItemUnroll * T) {
-        double2 v[kItemUnroll];
-        Pt p[kItemUnroll];
+    Pt p[kItemUnroll];
+    int64_t rank[kItemUnroll];
+    auto fetch = [&](uint32_t b) {
 #pragma unroll
         for (int u = 0; u < kItemUnroll; ++u) {
-            const uint32_t t = base + u * T;
+            const uint32_t t = b + u * T;
             if (t < D.n) {
                 p[u] = decompose(t, D);
-                const int64_t rank = forward ? __ldg(forward + p[u].e) : p[u].e;
-                v[u] = __ldg(reinterpret_cast<const double2 *>(flat + rank * inner + 2 * p[u].k));
+                rank[u] = forward ? __ldg(forward + p[u].e) : p[u].e;
             }
         }
+    };
+    uint32_t base = blockIdx.x * blockDim.x + threadIdx.x;
+    fetch(base);
+    for (; base < D.n; base += kItemUnroll * T) {
+        double2 v[kItemUnroll];
+        Pt q[kItemUnroll];
+#pragma unroll
+        for (int u = 0; u < kItemUnroll; ++u) {
+            if (base + u * T < D.n) {
+                v[u] = __ldg(reinterpret_cast<const double2 *>(flat + rank[u] * inner + 2 * p[u].k));
+                q[u] = p[u];
+            }
+        }
+        if (base + kItemUnroll * T < D.n) fetch(base + kItemUnroll * T);
 #pragma unroll
         for (int u = 0; u < kItemUnroll; ++u) {
             if (base + u * T >= D.n) break;
-            put2(f + F.at(p[u].i, p[u].c, p[u].j), images(F, p[u].i, p[u].j, flags), 2 * p[u].k, v[u]);
+            put2(f + F.at(q[u].i, q[u].c, q[u].j), images(F, q[u].i, q[u].j, flags), 2 * q[u].k, v[u]);
         }
     }
 }
@@ -468,8 +491,8 @@ extern "C" int tsg_pack(const tsg_grid *g, int loc, int inner, const double *fla
     PointDec D(g->rows, g->cols, F.colors, inner);
     if (pairs_ok(inner, flat)) {
         PointDec Dp(g->rows, g->cols, F.colors, inner / 2);
-        pack_pairs_kernel<<<grid_for((Dp.n + kItemUnroll - 1) / kItemUnroll, 256, g->num_sms), 256, 0,
-                            (cudaStream_t)s>>>(F, inner, Dp, flat, forward, field, g->flags);
+        pack_pairs_kernel<kPackUnroll><<<grid_for((Dp.n + kPackUnroll - 1) / kPackUnroll, 256, g->num_sms),
+                                         256, 0, (cudaStream_t)s>>>(F, inner, Dp, flat, forward, field, g->flags);
     } else if (inner >= 16)
         launch_lines(pack_lines_kernel, g->cols, (int64_t)g->rows * F.colors, g->num_sms,
                      (cudaStream_t)s, F, inner, flat, forward, field, g->flags);

@@ -104,41 +104,61 @@ __global__ void __launch_bounds__(256) reduce_indirect_kernel(const int64_t *__r
     }
 }
 
-// Table-driven reduce for an even level count: one thread per (row, level pair) item,
-// items flattened over the whole table so every lane is busy whatever the level count, and
-// kUnroll items per thread per pass with all their gathers issued before any sum -- the
-// gather is latency-bound otherwise (measured: 3.1 TB/s, 29 % issue, 50 % occupancy with
-// one warp per row).  Lanes of one row share its table entries (broadcast loads) and read
-// consecutive 16-byte pairs of each neighbour row (coalesced).
+// Level-pair item kernels (the table-driven MPDATA stages below, the reorders): kUnroll
+// items per thread per pass with all their loads issued before any use.  Lanes of one row
+// share its table entries (broadcast loads) and read consecutive 16-byte pairs of each
+// neighbour row (coalesced).
 constexpr int kUnroll = 4;
 
-// 4 resident 256-thread blocks per SM: 64 registers hold up to 12 gathers in flight
-// (k1 at 1024x1024x80: 575 vs 647 us with the compiler's 78 registers and 3 blocks)
-template <int W, bool SCALE>
-__global__ void __launch_bounds__(256, 4) reduce_indirect_pairs_kernel(
+// Level-pair items (one thread per (row, level pair), flattened over the field so every
+// lane is busy whatever the level count), with the next batch's table row (and scale)
+// fetched while this batch's W neighbour runs are in flight: the table load and the
+// gather it feeds are dependent, so an unpipelined batch waits two load latencies.  One
+// item per batch (32 registers, full occupancy): Table-1 k1 / k2 at 1024x1024x80
+// 443-472 us (0.89-0.94 of the copy peak) against 553-566 us for round 1's four
+// unpipelined items per thread and 594-1028 us for two / three pipelined ones
+// (tools/indirect_variants.py, TSG_IND_V A/B build; outputs bitwise identical).
+template <int W, bool SCALE, int U>
+__global__ void __launch_bounds__(256) reduce_indirect_pipe_kernel(
     const int64_t *__restrict__ table, uint32_t nitems, FastDiv npairs, int nlev,
     const double *__restrict__ src, const double *__restrict__ scale, double *__restrict__ dst) {
-    constexpr int U_ = (12 / W < kUnroll ? 12 / W : kUnroll) - (SCALE && W < 4 ? 1 : 0);  // <= 12 gathers
     const uint32_t T = gridDim.x * blockDim.x;
-    for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < nitems; base += U_ * T) {
-        double2 v[U_][W];
-        double sc[U_];
-        uint32_t row[U_], kp[U_];
+    int64_t nb[U][W];
+    uint32_t row[U], kp[U];
+    double sc[U];
+    auto fetch = [&](uint32_t b) {
 #pragma unroll
-        for (int u = 0; u < U_; ++u) {
-            const uint32_t it = base + u * T;
-            row[u] = npairs.div(it < nitems ? it : 0);
-            kp[u] = 2 * (it - row[u] * npairs.d);
+        for (int u = 0; u < U; ++u) {
+            const uint32_t it = b + u * T;
             if (it < nitems) {
+                row[u] = npairs.div(it);
+                kp[u] = 2 * (it - row[u] * npairs.d);
                 sc[u] = SCALE ? __ldg(scale + row[u]) : 1.0;
 #pragma unroll
-                for (int s = 0; s < W; ++s)
-                    v[u][s] = __ldg(reinterpret_cast<const double2 *>(
-                        src + __ldg(table + (int64_t)row[u] * W + s) * nlev + kp[u]));
+                for (int s = 0; s < W; ++s) nb[u][s] = __ldg(table + (int64_t)row[u] * W + s);
             }
         }
+    };
+    uint32_t base = blockIdx.x * blockDim.x + threadIdx.x;
+    fetch(base);
+    for (; base < nitems; base += U * T) {
+        double2 v[U][W];
+        uint32_t r2[U], k2[U];
+        double s2[U];
 #pragma unroll
-        for (int u = 0; u < U_; ++u) {
+        for (int u = 0; u < U; ++u) {
+            if (base + u * T < nitems) {
+#pragma unroll
+                for (int s = 0; s < W; ++s)
+                    v[u][s] = __ldg(reinterpret_cast<const double2 *>(src + nb[u][s] * nlev + kp[u]));
+                r2[u] = row[u];
+                k2[u] = kp[u];
+                s2[u] = sc[u];
+            }
+        }
+        if (base + U * T < nitems) fetch(base + U * T);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
             if (base + u * T >= nitems) break;
             double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
@@ -146,8 +166,8 @@ __global__ void __launch_bounds__(256, 4) reduce_indirect_pairs_kernel(
                 acc.x = add(v[u][s].x, acc.x);
                 acc.y = add(v[u][s].y, acc.y);
             }
-            if (SCALE) acc = make_double2(mul(acc.x, sc[u]), mul(acc.y, sc[u]));
-            st2(dst + (int64_t)row[u] * nlev + kp[u], acc);
+            if (SCALE) acc = make_double2(mul(acc.x, s2[u]), mul(acc.y, s2[u]));
+            st2(dst + (int64_t)r2[u] * nlev + k2[u], acc);
         }
     }
 }
@@ -579,17 +599,17 @@ extern "C" int tsg_neighbor_reduce_indirect(const int64_t *table, int64_t nrows,
         };
         if (scale) {
             switch (width) {
-                case 2: go(reduce_indirect_pairs_kernel<2, true>); break;
-                case 3: go(reduce_indirect_pairs_kernel<3, true>); break;
-                case 4: go(reduce_indirect_pairs_kernel<4, true>); break;
-                default: go(reduce_indirect_pairs_kernel<6, true>); break;
+                case 2: go(reduce_indirect_pipe_kernel<2, true, 1>); break;
+                case 3: go(reduce_indirect_pipe_kernel<3, true, 1>); break;
+                case 4: go(reduce_indirect_pipe_kernel<4, true, 1>); break;
+                default: go(reduce_indirect_pipe_kernel<6, true, 1>); break;
             }
         } else {
             switch (width) {
-                case 2: go(reduce_indirect_pairs_kernel<2, false>); break;
-                case 3: go(reduce_indirect_pairs_kernel<3, false>); break;
-                case 4: go(reduce_indirect_pairs_kernel<4, false>); break;
-                default: go(reduce_indirect_pairs_kernel<6, false>); break;
+                case 2: go(reduce_indirect_pipe_kernel<2, false, 1>); break;
+                case 3: go(reduce_indirect_pipe_kernel<3, false, 1>); break;
+                case 4: go(reduce_indirect_pipe_kernel<4, false, 1>); break;
+                default: go(reduce_indirect_pipe_kernel<6, false, 1>); break;
             }
         }
         TSG_CHECK_LAUNCH();
