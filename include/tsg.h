@@ -199,6 +199,27 @@ int tsg_transport_indirect(const int64_t *e2v, const int64_t *v2e, const double 
                            const double *wn, const double *rho, int64_t nv, int64_t ne,
                            int nlev, double dt, double pivbz, int flux_op, double *flux,
                            double *fluz, double *div, double *pd_out, tsg_stream s);
+/* The reference's flat stages one at a time (reference.py:18-90, 119-134; the per-stage
+ * functions beside transport_step), any numbering, row-major [element, level] arrays:
+ *   tsg_flat_flux             upwind_flux / centred_flux: e2v [ne,2] -> flux [ne,nlev]
+ *   tsg_flat_fluz             upwind_fluz: pd [nv,nlev], wn [nv,nlev+1] -> fluz [nv,nlev+1]
+ *                             (TSG_EVALUE below 2 levels, as the reference's ValueError)
+ *   tsg_flat_divergence       flux_divergence: v2e / signs [nv,width], dual [nv] -> div
+ *   tsg_flat_advance          advance_density over n = nv*nlev values
+ *   tsg_flat_cell_divergence  cell_divergence: c2e [nc,width], vn [ne,nlev], length [ne],
+ *                             area [nc] -> out [nc,nlev]
+ * Table ids are not bounds-checked here (the Python mirror checks them). */
+int tsg_flat_flux(const int64_t *e2v, const double *pd, const double *vn, int64_t ne, int nlev,
+                  int flux_op, double *flux, tsg_stream s);
+int tsg_flat_fluz(const double *pd, const double *wn, int64_t nv, int nlev, double pivbz,
+                  double *fluz, tsg_stream s);
+int tsg_flat_divergence(const int64_t *v2e, int width, const double *signs, const double *dual,
+                        const double *flux, const double *fluz, int64_t nv, int nlev, double *div,
+                        tsg_stream s);
+int tsg_flat_advance(const double *pd, const double *div, const double *rho, int64_t n, double dt,
+                     double *pd_out, tsg_stream s);
+int tsg_flat_cell_divergence(const int64_t *c2e, int width, const double *vn, const double *length,
+                             const double *area, int64_t nc, int nlev, double *out, tsg_stream s);
 /* Select the fused kernel's tile variant; 0 (the default) chooses per launch: the compact
  * 4x16 level-pair tile with a producer warp (variant 21: 512 compute threads + 32) when
  * the tile above a tile is still in L2 under the contiguous schedule or the band schedule

@@ -84,6 +84,7 @@ from .kernels import (
 )
 from .flat import StructuredStepper, transport_step, transport_step_structured
 from .traffic import TrafficReport, TrafficRow
+from . import reference  # the flat stage API of tristencil.reference
 
 UNFUSED_PLANE_WEIGHTS = {"nodes": (7, 3), "edges": (1, 1)}  # bench.py:57-60
 FUSED_PLANE_WEIGHTS = {"nodes": (4, 1)}

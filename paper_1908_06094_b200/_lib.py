@@ -68,6 +68,11 @@ SIGNATURES = {
     "tsg_fused_variant_info": (_c_int, [_c_int] + [ctypes.POINTER(_c_int)] * 6),
     "tsg_neighbor_reduce": (_c_int, [_p, _c_int, _c_int, _c_int, _p, _p, _p, _p]),
     "tsg_neighbor_reduce_indirect": (_c_int, [_p, _c_i64, _c_int, _c_int, _p, _p, _p, _p]),
+    "tsg_flat_flux": (_c_int, [_p, _p, _p, _c_i64, _c_int, _c_int, _p, _p]),
+    "tsg_flat_fluz": (_c_int, [_p, _p, _c_i64, _c_int, _c_dbl, _p, _p]),
+    "tsg_flat_divergence": (_c_int, [_p, _c_int, _p, _p, _p, _p, _c_i64, _c_int, _p, _p]),
+    "tsg_flat_advance": (_c_int, [_p, _p, _p, _c_i64, _c_dbl, _p, _p]),
+    "tsg_flat_cell_divergence": (_c_int, [_p, _c_int, _p, _p, _p, _c_i64, _c_int, _p, _p]),
     "tsg_cell_divergence": (_c_int, [_p, _c_int, _p, _p, _p, _p, _p, _p]),
     "tsg_cell_weights": (_c_int, [_p, _p, _p, _p, _p]),
     "tsg_build_neighbor_table": (_c_int, [_c_int, _c_int, _c_int, _c_int, _p, _p, _p, _p]),

@@ -420,6 +420,58 @@ __global__ void __launch_bounds__(256) ifluz_kernel(int64_t nv, int K, double pi
     }
 }
 
+// The reference's flat stages one by one (reference.py:18-90, 119-134), for callers of
+// its per-stage functions: the divergence over a table of any width, the explicit update,
+// and the table-driven cell divergence.  Same operation order as the fused kernels.
+__global__ void __launch_bounds__(256) idiv_kernel(const int64_t *__restrict__ v2e, int W, int64_t nv, int K,
+                                                   const double *__restrict__ signs,
+                                                   const double *__restrict__ dual,
+                                                   const double *__restrict__ flux,
+                                                   const double *__restrict__ fluz,
+                                                   double *__restrict__ div) {
+    TSG_FLAT_ROWS(v, nv) {
+        const int64_t *row = v2e + v * W;
+        const double *sg = signs + v * W, *Z = fluz + v * (K + 1);
+        const double du = __ldg(dual + v);
+        for (int k = threadIdx.x; k < K; k += 32) {
+            double acc = 0.0;
+            for (int s = 0; s < W; ++s) acc = add(mul(__ldg(sg + s), flux[__ldg(row + s) * K + k]), acc);
+            acc = add(acc, sub(Z[k + 1], Z[k]));
+            div[v * K + k] = dvd(acc, du);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) advance_flat_kernel(int64_t n, double dt, const double *__restrict__ pd,
+                                                           const double *__restrict__ div,
+                                                           const double *__restrict__ rho,
+                                                           double *__restrict__ out) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        double slope = mul(dt, div[q]);
+        slope = dvd(slope, rho[q]);
+        out[q] = sub(pd[q], slope);
+    }
+}
+
+__global__ void __launch_bounds__(256) icell_div_kernel(const int64_t *__restrict__ c2e, int W, int64_t nc, int K,
+                                                        const double *__restrict__ vn,
+                                                        const double *__restrict__ length,
+                                                        const double *__restrict__ area,
+                                                        double *__restrict__ out) {
+    TSG_FLAT_ROWS(c, nc) {
+        const int64_t *row = c2e + c * W;
+        const double ar = __ldg(area + c);
+        for (int k = threadIdx.x; k < K; k += 32) {
+            double acc = 0.0;
+            for (int s = 0; s < W; ++s) {
+                const int64_t e = __ldg(row + s);
+                acc = add(mul(vn[e * K + k], __ldg(length + e)), acc);
+            }
+            out[c * K + k] = dvd(acc, ar);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) idiv_advance_kernel(
     const int64_t *__restrict__ v2e, int64_t nv, int K, double dt, const double *__restrict__ signs,
     const double *__restrict__ dual, const double *__restrict__ flux,
@@ -735,6 +787,80 @@ extern "C" int tsg_transport_indirect(const int64_t *e2v, const int64_t *v2e, co
     launch_rows(ifluz_kernel, nv, sms, st, nv, nlev, pivbz, pd, wn, fluz);
     launch_rows(idiv_advance_kernel, nv, sms, st, v2e, nv, nlev, dt, signs, dual, flux, fluz, pd, rho,
                 div, pd_out);
+    TSG_CHECK_LAUNCH();
+    return TSG_OK;
+}
+
+// -- the reference's flat stages one by one (reference.py:18-90, 119-134) ---------------
+
+extern "C" int tsg_flat_flux(const int64_t *e2v, const double *pd, const double *vn, int64_t ne, int nlev,
+                             int flux_op, double *flux, tsg_stream s) {
+    if (!e2v || !pd || !vn || !flux) return fail(TSG_EVALUE, "tsg_flat_flux: NULL array");
+    if (flux_op != TSG_UPWIND && flux_op != TSG_CENTRED) return fail(TSG_EVALUE, "unknown flux operator %d", flux_op);
+    if (ne < 0 || nlev < 1) return fail(TSG_EVALUE, "bad shape (ne=%lld, levels %d)", (long long)ne, nlev);
+    if (ne == 0) return TSG_OK;
+    cudaStream_t st = (cudaStream_t)s;
+    const int sms = sm_count();
+    auto a16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) % 16) == 0; };
+    if ((nlev & 1) == 0 && ne * (nlev / 2) < (1LL << 31) && a16(pd) && a16(vn) && a16(flux)) {
+        const int np = nlev / 2;
+        const uint32_t nE = (uint32_t)(ne * np);
+        const unsigned blocks = (unsigned)std::min<int64_t>(((int64_t)nE + 256 * kUnroll - 1) / (256 * kUnroll),
+                                                            (int64_t)sms * 8);
+        if (flux_op == TSG_UPWIND)
+            iflux_pairs_kernel<TSG_UPWIND><<<blocks, 256, 0, st>>>(e2v, nE, FastDiv(np), nlev, pd, vn, flux);
+        else
+            iflux_pairs_kernel<TSG_CENTRED><<<blocks, 256, 0, st>>>(e2v, nE, FastDiv(np), nlev, pd, vn, flux);
+    } else if (flux_op == TSG_UPWIND) {
+        launch_rows(iflux_kernel<TSG_UPWIND>, ne, sms, st, e2v, ne, nlev, pd, vn, flux);
+    } else {
+        launch_rows(iflux_kernel<TSG_CENTRED>, ne, sms, st, e2v, ne, nlev, pd, vn, flux);
+    }
+    TSG_CHECK_LAUNCH();
+    return TSG_OK;
+}
+
+extern "C" int tsg_flat_fluz(const double *pd, const double *wn, int64_t nv, int nlev, double pivbz, double *fluz,
+                             tsg_stream s) {
+    if (!pd || !wn || !fluz) return fail(TSG_EVALUE, "tsg_flat_fluz: NULL array");
+    if (nlev < 2) return fail(TSG_EVALUE, "need at least 2 levels, got %d", nlev);
+    if (nv < 0) return fail(TSG_EVALUE, "bad vertex count %lld", (long long)nv);
+    if (nv == 0) return TSG_OK;
+    launch_rows(ifluz_kernel, nv, sm_count(), (cudaStream_t)s, nv, nlev, pivbz, pd, wn, fluz);
+    TSG_CHECK_LAUNCH();
+    return TSG_OK;
+}
+
+extern "C" int tsg_flat_divergence(const int64_t *v2e, int width, const double *signs, const double *dual,
+                                   const double *flux, const double *fluz, int64_t nv, int nlev, double *div,
+                                   tsg_stream s) {
+    if (!v2e || !signs || !dual || !flux || !fluz || !div) return fail(TSG_EVALUE, "tsg_flat_divergence: NULL array");
+    if (nv < 0 || width < 0 || nlev < 1)
+        return fail(TSG_EVALUE, "bad shape (nv=%lld, width %d, levels %d)", (long long)nv, width, nlev);
+    if (nv == 0) return TSG_OK;
+    launch_rows(idiv_kernel, nv, sm_count(), (cudaStream_t)s, v2e, width, nv, nlev, signs, dual, flux, fluz, div);
+    TSG_CHECK_LAUNCH();
+    return TSG_OK;
+}
+
+extern "C" int tsg_flat_advance(const double *pd, const double *div, const double *rho, int64_t n, double dt,
+                                double *pd_out, tsg_stream s) {
+    if (!pd || !div || !rho || !pd_out) return fail(TSG_EVALUE, "tsg_flat_advance: NULL array");
+    if (n < 0) return fail(TSG_EVALUE, "bad value count %lld", (long long)n);
+    if (n == 0) return TSG_OK;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
+    advance_flat_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)s>>>(n, dt, pd, div, rho, pd_out);
+    TSG_CHECK_LAUNCH();
+    return TSG_OK;
+}
+
+extern "C" int tsg_flat_cell_divergence(const int64_t *c2e, int width, const double *vn, const double *length,
+                                        const double *area, int64_t nc, int nlev, double *out, tsg_stream s) {
+    if (!c2e || !vn || !length || !area || !out) return fail(TSG_EVALUE, "tsg_flat_cell_divergence: NULL array");
+    if (nc < 0 || width < 0 || nlev < 1)
+        return fail(TSG_EVALUE, "bad shape (nc=%lld, width %d, levels %d)", (long long)nc, width, nlev);
+    if (nc == 0) return TSG_OK;
+    launch_rows(icell_div_kernel, nc, sm_count(), (cudaStream_t)s, c2e, width, nc, nlev, vn, length, area, out);
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }
