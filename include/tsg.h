@@ -14,9 +14,11 @@
  *    `tsg_stream` is a cudaStream_t, every launch is stream-ordered and asynchronous.
  *  - Thread safety: calls are reentrant across grid handles; one grid handle is used by
  *    one host thread at a time (it caches the time loops' captured graph), and its fused
- *    launches are stream-ordered (they share the handle's work-deal counters: concurrent
- *    fused steps on one handle from two streams need two handles).  The tuning switches
- *    (tsg_set_fused_variant / _band / _schedule) are process-wide benchmarking hooks.
+ *    steps and its large neighbour reductions are stream-ordered (they share the handle's
+ *    work-deal counters: concurrent fused steps, or concurrent dynamically dealt reduces,
+ *    on one handle from two streams need two handles).  The tuning switches
+ *    (tsg_set_fused_variant / _band / _schedule, tsg_set_reduce_variant) are process-wide
+ *    benchmarking hooks.
  *  - Structured ("direct") fields live in the device layout
  *        double field[rows + 2][colors][cols + 2][tsg_inner_pitch(inner)]
  *    i.e. (row, colour, column) parallelogram indexing with a one-element periodic

@@ -32,6 +32,7 @@ import numpy as np
 
 from .layouts import AXES, LayoutSpec, LinearLayout
 from .topology import PatchSpec, as_location
+from .traffic import TrafficReport, TrafficRow  # noqa: F401  (storage.py:410-479 of the reference)
 
 SPACES = ("primary", "mirror")
 

@@ -1,2 +1,1 @@
-mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_gpu_reference_api.py -x -q 2>&1 | tail -15
+timeout 600 python tools/op_sustained_o1280.py
