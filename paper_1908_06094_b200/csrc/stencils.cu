@@ -526,6 +526,54 @@ __global__ void __launch_bounds__(256) iflux_pairs_kernel(const int64_t *__restr
     }
 }
 
+// The divergence + update stage with the next item's six table entries fetched while the
+// current item's flux rows are in flight (one item per thread, as the Table-1 gather
+// above: the table load and the gather it feeds are dependent loads).  279x256x80 step
+// 155.3 -> 149.0 us, 1024x1024x80 2112 -> 1993 us (tools/indirect_step_variants.py,
+// TSG_IPIPE A/B build, bitwise unchanged); the same for the two-row edge flux gather
+// lost (157.4 / 2126 us), so that stage keeps four items per thread.
+__global__ void __launch_bounds__(256) idiv_advance_pipe_kernel(
+    const int64_t *__restrict__ v2e, uint32_t n, FastDiv np, int K, double dt,
+    const double *__restrict__ signs, const double *__restrict__ dual, const double *__restrict__ flux,
+    const double *__restrict__ fluz, const double *__restrict__ pd, const double *__restrict__ rho,
+    double *__restrict__ div, double *__restrict__ pd_out) {
+    const uint32_t T = gridDim.x * blockDim.x;
+    uint32_t it = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t v = 0;
+    int64_t nb[6];
+    auto fetch = [&](uint32_t i) {
+        v = np.div(i);
+#pragma unroll
+        for (int s = 0; s < 6; ++s) nb[s] = __ldg(v2e + (int64_t)v * 6 + s);
+    };
+    if (it < n) fetch(it);
+    for (; it < n; it += T) {
+        const int k = 2 * (it - v * np.d);
+        const uint32_t vc = v;
+        double2 f[6];
+#pragma unroll
+        for (int s = 0; s < 6; ++s) f[s] = ld2(flux + nb[s] * K + k);
+        if (it + T < n) fetch(it + T);
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int s = 0; s < 6; ++s) {
+            const double sg = __ldg(signs + (int64_t)vc * 6 + s);
+            acc.x = add(mul(sg, f[s].x), acc.x);
+            acc.y = add(mul(sg, f[s].y), acc.y);
+        }
+        const double *Z = fluz + (int64_t)vc * (K + 1) + k;  // odd row width: scalar loads
+        const double z0 = Z[0], z1 = Z[1], z2 = Z[2];
+        acc.x = add(acc.x, sub(z1, z0));
+        acc.y = add(acc.y, sub(z2, z1));
+        const double du = __ldg(dual + vc);
+        const double2 d = make_double2(dvd(acc.x, du), dvd(acc.y, du));
+        const int64_t qq = (int64_t)vc * K + k;
+        st2(div + qq, d);
+        const double2 r = ld2(rho + qq), p = ld2(pd + qq);
+        st2(pd_out + qq, make_double2(sub(p.x, dvd(mul(dt, d.x), r.x)), sub(p.y, dvd(mul(dt, d.y), r.y))));
+    }
+}
+
 // interfaces in pairs over 0..K of a K+1-wide row (odd width: the last item is a single)
 __global__ void __launch_bounds__(256) ifluz_pairs_kernel(uint32_t n, FastDiv np, int K, double pivbz,
                                                           const double *__restrict__ pd,
@@ -549,34 +597,6 @@ __global__ void __launch_bounds__(256) ifluz_pairs_kernel(uint32_t n, FastDiv np
     }
 }
 
-__global__ void __launch_bounds__(256) idiv_advance_pairs_kernel(
-    const int64_t *__restrict__ v2e, uint32_t n, FastDiv np, int K, double dt,
-    const double *__restrict__ signs, const double *__restrict__ dual, const double *__restrict__ flux,
-    const double *__restrict__ fluz, const double *__restrict__ pd, const double *__restrict__ rho,
-    double *__restrict__ div, double *__restrict__ pd_out) {
-    TSG_FLAT_ITEMS(it, u, n) {
-        const uint32_t v = np.div(it);
-        const int k = 2 * (it - v * np.d);
-        double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int s = 0; s < 6; ++s) {
-            const double2 f = ld2(flux + __ldg(v2e + (int64_t)v * 6 + s) * K + k);
-            const double sg = __ldg(signs + (int64_t)v * 6 + s);
-            acc.x = add(mul(sg, f.x), acc.x);
-            acc.y = add(mul(sg, f.y), acc.y);
-        }
-        const double *Z = fluz + (int64_t)v * (K + 1) + k;  // odd row width: scalar loads
-        const double z0 = Z[0], z1 = Z[1], z2 = Z[2];
-        acc.x = add(acc.x, sub(z1, z0));
-        acc.y = add(acc.y, sub(z2, z1));
-        const double du = __ldg(dual + v);
-        const double2 d = make_double2(dvd(acc.x, du), dvd(acc.y, du));
-        const int64_t q = (int64_t)v * K + k;
-        st2(div + q, d);
-        const double2 r = ld2(rho + q), p = ld2(pd + q);
-        st2(pd_out + q, make_double2(sub(p.x, dvd(mul(dt, d.x), r.x)), sub(p.y, dvd(mul(dt, d.y), r.y))));
-    }
-}
 #undef TSG_FLAT_ITEMS
 
 }  // namespace tsg
@@ -775,8 +795,9 @@ extern "C" int tsg_transport_indirect(const int64_t *e2v, const int64_t *v2e, co
         else
             iflux_pairs_kernel<TSG_CENTRED><<<blocks(nE), 256, 0, st>>>(e2v, nE, FastDiv(np), nlev, pd, vn, flux);
         ifluz_pairs_kernel<<<blocks(nZ), 256, 0, st>>>(nZ, FastDiv(np + 1), nlev, pivbz, pd, wn, fluz);
-        idiv_advance_pairs_kernel<<<blocks(nV), 256, 0, st>>>(v2e, nV, FastDiv(np), nlev, dt, signs, dual,
-                                                              flux, fluz, pd, rho, div, pd_out);
+        const unsigned bV = (unsigned)std::min<int64_t>(((int64_t)nV + 255) / 256, (int64_t)sms * 8);
+        idiv_advance_pipe_kernel<<<bV, 256, 0, st>>>(v2e, nV, FastDiv(np), nlev, dt, signs, dual, flux, fluz, pd,
+                                                     rho, div, pd_out);
         TSG_CHECK_LAUNCH();
         return TSG_OK;
     }

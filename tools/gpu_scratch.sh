@@ -1,1 +1,2 @@
-timeout 300 python tools/pcie_probe.py
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 300 python tools/indirect_step_variants.py
