@@ -1,3 +1,4 @@
-TSG_SHARE_ONE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 4 --steps 20 --warmup 3 > gpurun_out/bench4.log 2>&1
+CS=/usr/local/cuda/bin/compute-sanitizer
+timeout 2400 $CS --tool memcheck --print-limit 5 python -m pytest tests/test_gpu_reference_api.py tests/test_gpu_acceptance.py "tests/test_gpu_api.py::test_pack_unpack_roundtrip_every_numbering" "tests/test_gpu_api.py::test_table1_kernels_direct_and_indirect" "tests/test_gpu_api.py::test_relabelled_flat_paths_are_invariant" "tests/test_gpu_api.py::test_indirect_reduce_every_width" -q -x > gpurun_out/memcheck_r2.log 2>&1
 echo rc=$?
-tail -c 2500 gpurun_out/bench4.log
+grep -v "^=========     \(#\|in \|Saved\)" gpurun_out/memcheck_r2.log | tail -8
