@@ -196,17 +196,23 @@ def cpu_record(w: dict, times, threads) -> dict:
 
 
 def reference_python_record(w: dict, reps: int) -> dict | None:
-    """The reference package itself (baseline/_ref, unmodified): its fastest CPU path,
-    ``run_fused(comp, TileSpec(R, C, 1))`` via its own ``time_computation`` (median), on
-    ``_transport_setup`` inputs (bench.py:293-303, :386-397)."""
+    """The reference package itself (baseline/_ref, unmodified), its three CPU paths on
+    ``_transport_setup`` inputs (bench.py:293-303, :375-427): the
+    fastest, ``run_fused(comp, TileSpec(R, C, 1))`` via its own ``time_computation``
+    (median of ``reps``), plus ``run_naive`` and the flat oracle ``reference.transport_step``
+    (one timed run each after one warm-up; table building outside the timing)."""
     ref = ROOT / "baseline" / "_ref"
     if not (ref / "tristencil").is_dir():
         return None
     sys.path.insert(0, str(ref))
     try:
         from tristencil import mpdata as rmp
+        from tristencil import reference as rref
         from tristencil.bench import BenchConfig, _transport_setup
-        from tristencil.executors import TileSpec, time_computation, run_fused
+        from tristencil.connectivity import build_neighbor_table, edge_signs_table
+        from tristencil.executors import TileSpec, time_computation, run_fused, run_naive
+        from tristencil.kernels import field_to_flat
+        from tristencil.topology import LocationType
     finally:
         sys.path.remove(str(ref))
     r, c, k = w["cpu_rows"], w["cols"], w["levels"]
@@ -216,11 +222,24 @@ def reference_python_record(w: dict, reps: int) -> dict | None:
     comp = rmp.build_mpdata(spec, state, geo, params)
     tiles = TileSpec(r, c, 1)
     timing = time_computation(comp, lambda cc: run_fused(cc, tiles), reps=reps, warmup=1)
-    return {"value": r * c * k / timing.median_seconds, "unit": UNIT, "cores": 1,
+    naive = time_computation(comp, run_naive, reps=1, warmup=1)
+    E, V = LocationType.EDGES, LocationType.VERTICES
+    args = (build_neighbor_table(spec, E, V).ids, build_neighbor_table(spec, V, E).ids, edge_signs_table(spec),
+            field_to_flat(geo.dual_volumes)[:, 0], field_to_flat(state.pd_in), field_to_flat(state.vn),
+            field_to_flat(state.wn), field_to_flat(state.rho), params.dt, params.pivbz)
+    rref.transport_step(*args)
+    t0 = time.perf_counter()
+    rref.transport_step(*args)
+    t_oracle = time.perf_counter() - t0
+    vk = r * c * k
+    return {"value": vk / timing.median_seconds, "unit": UNIT, "cores": 1,
             "kind": "reference-python", "ms_per_step": timing.median_seconds * 1e3,
             "reference_updates_per_second": 1.0 / timing.seconds_per_update,
             "sample": f"{r}x{c}x{k} patch, tristencil.run_fused(comp, TileSpec({r}, {c}, 1)) "
-                      f"(its fastest path), median of {reps} via its time_computation"}
+                      f"(its fastest path), median of {reps} via its time_computation",
+            "run_naive": {"value": vk / naive.median_seconds, "ms_per_step": naive.median_seconds * 1e3},
+            "transport_step": {"value": vk / t_oracle, "ms_per_step": t_oracle * 1e3,
+                               "note": "reference.transport_step, the flat oracle (tables built outside)"}}
 
 
 def cpu_baseline(args, w: dict) -> dict:
@@ -252,7 +271,9 @@ def run_reference(args):
         "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    if not args.no_python_ref:
+    # the package itself on the cfg3 patch only: its O1280 sample (a 320-row strip) would
+    # take ~80 s per step in pure Python
+    if not args.no_python_ref and args.workload == "cfg3":
         try:
             line["reference_python"] = reference_python_record(w, args.python_ref_reps)
         except Exception as e:  # the record is informational: never lose the line over it
