@@ -609,7 +609,10 @@ def run_ours(args):
                            "one launch per step replayed as a captured two-step CUDA graph"}
             del st
             torch.cuda.empty_cache()
-            e2e_loop = e2e_time_loop(w, max(5, min(args.steps, 20)))
+            try:  # informational beside e2e: never lose the line over it
+                e2e_loop = e2e_time_loop(w, max(5, min(args.steps, 20)))
+            except Exception as exc:  # noqa: BLE001
+                e2e_loop = {"unavailable": f"{type(exc).__name__}: {exc}"}
         o1280 = None
         if args.workload == "cfg3" and not args.no_o1280:
             o1280 = o1280_strong(args, rank, world, shared, barrier, peak)
