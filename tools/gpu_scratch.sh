@@ -1,2 +1,3 @@
-timeout 600 python tools/reduce_variants.py 256 256 80 0,6,7,9 2>&1 | grep -v '"variant": 1[0-9]'
-timeout 600 python tools/reduce_variants.py 128 128 80 0,6,7,9 2>&1 | grep "VV\|CV\|EV"
+mkdir -p gpurun_out
+timeout 900 python tools/bench_stencils.py r2c > gpurun_out/stencils_r2c.log 2>&1
+tail -2 gpurun_out/stencils_r2c.log
