@@ -170,7 +170,7 @@ def cpu_port_sample(rows: int, cols: int, levels: int, warmup: int, steps: int |
     v2e = O.neighbor_table(rows, cols, "vertices", "edges")
     args = (e2v, v2e, inp["signs"], inp["dual"], inp["pd"], inp["vn"], inp["wn"], inp["rho"], DT, PIVBZ)
     out = None
-    for _ in range(warmup):
+    for _ in range(max(warmup, 1)):
         out = c_oracle.transport_step(*args, out=out)
     times = []
     t_begin = time.perf_counter()
@@ -182,7 +182,7 @@ def cpu_port_sample(rows: int, cols: int, levels: int, warmup: int, steps: int |
             break
         if budget_s is not None and time.perf_counter() - t_begin > budget_s and len(times) >= 3:
             break
-    return times, c_oracle.threads()
+    return times, c_oracle.threads(), out["pd_out"].copy()
 
 
 def cpu_record(w: dict, times, threads) -> dict:
@@ -242,15 +242,19 @@ def reference_python_record(w: dict, reps: int) -> dict | None:
                                "note": "reference.transport_step, the flat oracle (tables built outside)"}}
 
 
+CPU_PD_OUT = {}
+
+
 def cpu_baseline(args, w: dict) -> dict:
     """The one CPU-baseline protocol both arms use: the C port on every host core,
     ``--warmup`` untimed steps, then ``--steps`` timed ones (3 for the O1280 sample) capped
     at ``--cpu-seconds``, median; run before any CUDA work in the process."""
     steps = args.steps if args.workload == "cfg3" else min(args.steps, 3)
-    times, threads = cpu_port_sample(w["cpu_rows"], w["cols"], w["levels"], args.warmup, steps=steps,
-                                     budget_s=args.cpu_seconds)
+    times, threads, pd_out = cpu_port_sample(w["cpu_rows"], w["cols"], w["levels"], args.warmup, steps=steps,
+                                             budget_s=args.cpu_seconds)
     rec = cpu_record(w, times, threads)
     rec["steps"] = len(times)
+    CPU_PD_OUT[args.workload] = pd_out  # the sample's own result: the GPU's is checked against it
     return rec
 
 
@@ -565,6 +569,13 @@ def run_ours(args):
             sig = transport_inputs(w["rows"], cols, K, 0, "uniform", "gaussian-bump", "one")["signs"]
             st.set_geometry(sig, inp["dual"])
             st.upload(inp["pd"], inp["vn"], inp["wn"], inp["rho"])
+            if cpu is not None and "cfg3" in CPU_PD_OUT:
+                # the benchmarked kernel's result on these inputs against the CPU sample's own
+                st.step(DT, PIVBZ)
+                cpu["gpu_parity"] = {
+                    "bitwise": bool(np.array_equal(st.download(), CPU_PD_OUT["cfg3"])),
+                    "checked": "pd_out of one fused step (tsg_mpdata_step, dynamic deal) on the "
+                               "benchmarked inputs vs the C port's result in this sample"}
             pinned = [torch.from_numpy(np.ascontiguousarray(inp[n])).pin_memory()
                       for n in ("pd", "vn", "wn", "rho")]
             outs = [torch.empty((V, K), dtype=torch.float64).pin_memory() for _ in range(2)]
