@@ -106,6 +106,19 @@ int tsg_pack_strided(const tsg_grid *g, int loc, int inner, const double *src,
                      const int64_t *layout6, int host_halo, double *field, tsg_stream s);
 int tsg_unpack_strided(const tsg_grid *g, int loc, int inner, const double *field,
                        const int64_t *layout6, int host_halo, double *dst, tsg_stream s);
+/* The same for a band of rows, so a host field can be streamed through the step band by
+ * band (executors.run_fused on host Fields): pack logical rows [row_lo, row_hi) (with
+ * their halo images), unpack host storage rows [srow_lo, srow_hi) of 0 .. rows + 2h. */
+int tsg_pack_strided_rows(const tsg_grid *g, int loc, int inner, const double *src,
+                          const int64_t *layout6, int host_halo, int row_lo, int row_hi,
+                          double *field, tsg_stream s);
+int tsg_unpack_strided_rows(const tsg_grid *g, int loc, int inner, const double *field,
+                            const int64_t *layout6, int host_halo, int srow_lo, int srow_hi,
+                            double *dst, tsg_stream s);
+/* cudaMemcpy2DAsync of `height` rows of `width` bytes (kind 1 = H2D, 2 = D2H): one band
+ * of storage rows of a level-outer host layout per call. */
+int tsg_memcpy2d(void *dst, int64_t dpitch, const void *src, int64_t spitch, int64_t width,
+                 int64_t height, int kind, tsg_stream s);
 
 /* ---- MPDATA transport step (mpdata.py:189-354; reference.py:93-116) ---------------- */
 /* Fused single-pass step: flux -> fluz -> divergence -> advance with every intermediate

@@ -33,6 +33,11 @@ SIGNATURES = {
     "tsg_unpack": (_c_int, [_p, _c_int, _c_int, _p, _p, _p, _p]),
     "tsg_pack_strided": (_c_int, [_p, _c_int, _c_int, _p, ctypes.POINTER(_c_i64), _c_int, _p, _p]),
     "tsg_unpack_strided": (_c_int, [_p, _c_int, _c_int, _p, ctypes.POINTER(_c_i64), _c_int, _p, _p]),
+    "tsg_pack_strided_rows": (_c_int, [_p, _c_int, _c_int, _p, ctypes.POINTER(_c_i64), _c_int, _c_int, _c_int,
+                                       _p, _p]),
+    "tsg_unpack_strided_rows": (_c_int, [_p, _c_int, _c_int, _p, ctypes.POINTER(_c_i64), _c_int, _c_int,
+                                         _c_int, _p, _p]),
+    "tsg_memcpy2d": (_c_int, [_p, _c_i64, _p, _c_i64, _c_i64, _c_i64, _c_int, _p]),
     "tsg_mpdata_step": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _c_dbl, _c_dbl, _c_int, _p]),
     "tsg_mpdata_step_rows": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _c_dbl, _c_dbl, _c_int, _c_int,
                                       _c_int, _p]),

@@ -308,10 +308,11 @@ struct HostLayout {
     int64_t front, s[5];
 };
 
+// rows [i0, i1) of the field (the whole field, or one band of a streamed upload)
 __global__ void pack_strided_kernel(FieldIx F, int inner, int inner_is_level, HostLayout L, int h,
                                     const double *__restrict__ src, double *__restrict__ f,
-                                    int flags) {
-    const int64_t n = (int64_t)F.rows * F.colors * F.cols * inner;
+                                    int flags, int i0, int i1) {
+    const int64_t n = (int64_t)(i1 - i0) * F.colors * F.cols * inner;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
          t += (int64_t)gridDim.x * blockDim.x) {
         int64_t id = t / inner;
@@ -319,18 +320,19 @@ __global__ void pack_strided_kernel(FieldIx F, int inner, int inner_is_level, Ho
         int j = (int)(id % F.cols);
         int64_t rest = id / F.cols;
         int c = (int)(rest % F.colors);
-        int i = (int)(rest / F.colors);
+        int i = i0 + (int)(rest / F.colors);
         int64_t off = L.front + (int64_t)(i + h) * L.s[0] + (int64_t)c * L.s[1] +
                       (int64_t)(j + h) * L.s[2] + (int64_t)q * L.s[inner_is_level ? 3 : 4];
         store_img(f, F, i, c, j, q, src[off], flags);
     }
 }
 
+// host storage rows [s0, s1) (halo rows included: 0 .. rows + 2h)
 __global__ void unpack_strided_kernel(FieldIx F, int inner, int inner_is_level, HostLayout L,
                                       int h, const double *__restrict__ f,
-                                      double *__restrict__ dst) {
-    const int R = F.rows + 2 * h, Cc = F.cols + 2 * h;
-    const int64_t n = (int64_t)R * F.colors * Cc * inner;
+                                      double *__restrict__ dst, int s0, int s1) {
+    const int Cc = F.cols + 2 * h;
+    const int64_t n = (int64_t)(s1 - s0) * F.colors * Cc * inner;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
          t += (int64_t)gridDim.x * blockDim.x) {
         int64_t id = t / inner;
@@ -338,7 +340,7 @@ __global__ void unpack_strided_kernel(FieldIx F, int inner, int inner_is_level, 
         int sj = (int)(id % Cc);
         int64_t rest = id / Cc;
         int c = (int)(rest % F.colors);
-        int si = (int)(rest / F.colors);
+        int si = s0 + (int)(rest / F.colors);
         // host halo cells are periodic images of the interior
         int i = ((si - h) % F.rows + F.rows) % F.rows, j = ((sj - h) % F.cols + F.cols) % F.cols;
         int64_t off = L.front + (int64_t)si * L.s[0] + (int64_t)c * L.s[1] + (int64_t)sj * L.s[2] +
@@ -601,19 +603,52 @@ static int to_layout(const int64_t *lay, HostLayout &L) {
     return TSG_OK;
 }
 
-extern "C" int tsg_pack_strided(const tsg_grid *g, int loc, int inner, const double *src,
-                                const int64_t *layout6, int host_halo, double *field, tsg_stream s) {
+extern "C" int tsg_pack_strided_rows(const tsg_grid *g, int loc, int inner, const double *src,
+                                     const int64_t *layout6, int host_halo, int row_lo, int row_hi,
+                                     double *field, tsg_stream s) {
     CHECK_GRID(g);
     if (!valid_loc(loc) || inner < 1) return fail(TSG_EVALUE, "tsg_pack_strided: bad location/inner");
     if (!src || !field) return fail(TSG_EVALUE, "tsg_pack_strided: NULL array");
+    if (row_lo < 0 || row_hi > g->rows || row_lo > row_hi)
+        return fail(TSG_EVALUE, "row range [%d, %d) outside [0, %d)", row_lo, row_hi, g->rows);
     HostLayout L;
     if (int rc = to_layout(layout6, L)) return rc;
     // inner runs along `level` when the level stride is set, else along `extra`
     int inner_is_level = inner == 1 ? 1 : (L.s[3] != 0);
     FieldIx F(g->rows, g->cols, colors_of(loc), inner);
-    int64_t n = (int64_t)g->rows * F.colors * g->cols * inner;
+    int64_t n = (int64_t)(row_hi - row_lo) * F.colors * g->cols * inner;
+    if (n == 0) return TSG_OK;
     pack_strided_kernel<<<grid_for(n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(
-        F, inner, inner_is_level, L, host_halo, src, field, g->flags);
+        F, inner, inner_is_level, L, host_halo, src, field, g->flags, row_lo, row_hi);
+    TSG_CHECK_LAUNCH();
+    return TSG_OK;
+}
+
+extern "C" int tsg_pack_strided(const tsg_grid *g, int loc, int inner, const double *src,
+                                const int64_t *layout6, int host_halo, double *field, tsg_stream s) {
+    CHECK_GRID(g);
+    return tsg_pack_strided_rows(g, loc, inner, src, layout6, host_halo, 0, g->rows, field, s);
+}
+
+extern "C" int tsg_unpack_strided_rows(const tsg_grid *g, int loc, int inner, const double *field,
+                                       const int64_t *layout6, int host_halo, int srow_lo, int srow_hi,
+                                       double *dst, tsg_stream s) {
+    CHECK_GRID(g);
+    if (!valid_loc(loc) || inner < 1) return fail(TSG_EVALUE, "tsg_unpack_strided: bad location/inner");
+    if (!dst || !field) return fail(TSG_EVALUE, "tsg_unpack_strided: NULL array");
+    if (host_halo < 0 || host_halo > g->rows || host_halo > g->cols)
+        return fail(TSG_EVALUE, "host halo %d out of range", host_halo);
+    if (srow_lo < 0 || srow_hi > g->rows + 2 * host_halo || srow_lo > srow_hi)
+        return fail(TSG_EVALUE, "storage row range [%d, %d) outside [0, %d)", srow_lo, srow_hi,
+                    g->rows + 2 * host_halo);
+    HostLayout L;
+    if (int rc = to_layout(layout6, L)) return rc;
+    int inner_is_level = inner == 1 ? 1 : (L.s[3] != 0);
+    FieldIx F(g->rows, g->cols, colors_of(loc), inner);
+    int64_t n = (int64_t)(srow_hi - srow_lo) * F.colors * (g->cols + 2 * host_halo) * inner;
+    if (n == 0) return TSG_OK;
+    unpack_strided_kernel<<<grid_for(n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(
+        F, inner, inner_is_level, L, host_halo, field, dst, srow_lo, srow_hi);
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }
@@ -621,19 +656,8 @@ extern "C" int tsg_pack_strided(const tsg_grid *g, int loc, int inner, const dou
 extern "C" int tsg_unpack_strided(const tsg_grid *g, int loc, int inner, const double *field,
                                   const int64_t *layout6, int host_halo, double *dst, tsg_stream s) {
     CHECK_GRID(g);
-    if (!valid_loc(loc) || inner < 1) return fail(TSG_EVALUE, "tsg_unpack_strided: bad location/inner");
-    if (!dst || !field) return fail(TSG_EVALUE, "tsg_unpack_strided: NULL array");
-    if (host_halo < 0 || host_halo > g->rows || host_halo > g->cols)
-        return fail(TSG_EVALUE, "host halo %d out of range", host_halo);
-    HostLayout L;
-    if (int rc = to_layout(layout6, L)) return rc;
-    int inner_is_level = inner == 1 ? 1 : (L.s[3] != 0);
-    FieldIx F(g->rows, g->cols, colors_of(loc), inner);
-    int64_t n = (int64_t)(g->rows + 2 * host_halo) * F.colors * (g->cols + 2 * host_halo) * inner;
-    unpack_strided_kernel<<<grid_for(n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(
-        F, inner, inner_is_level, L, host_halo, field, dst);
-    TSG_CHECK_LAUNCH();
-    return TSG_OK;
+    return tsg_unpack_strided_rows(g, loc, inner, field, layout6, host_halo, 0, g->rows + 2 * host_halo,
+                                   dst, s);
 }
 
 extern "C" int tsg_cell_weights(const tsg_grid *g, const double *length, const double *area,
@@ -686,5 +710,21 @@ extern "C" int tsg_make_permutation(int rows, int cols, int loc, int numbering, 
     hilbert_write_kernel<<<(unsigned)nb, kHilbertBlock, 0, st>>>(side, gx, gy, cols,
                                                                  loc == TSG_CELLS, work, forward);
     TSG_CHECK_LAUNCH();
+    return TSG_OK;
+}
+
+// Strided host <-> device copy of `height` rows of `width` bytes (cudaMemcpy2DAsync): one
+// band of storage rows of a level-outer host layout is one such copy (executors.py's
+// streamed run_fused).  kind 1 = host to device, 2 = device to host.
+extern "C" int tsg_memcpy2d(void *dst, int64_t dpitch, const void *src, int64_t spitch, int64_t width,
+                            int64_t height, int kind, tsg_stream s) {
+    if (!dst || !src) return fail(TSG_EVALUE, "tsg_memcpy2d: NULL pointer");
+    if (kind != 1 && kind != 2) return fail(TSG_EVALUE, "tsg_memcpy2d: kind must be 1 (H2D) or 2 (D2H)");
+    if (width < 0 || height < 0 || dpitch < width || spitch < width)
+        return fail(TSG_EVALUE, "tsg_memcpy2d: bad extents");
+    if (width == 0 || height == 0) return TSG_OK;
+    TSG_CHECK_CUDA(cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width, (size_t)height,
+                                     kind == 1 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
+                                     (cudaStream_t)s));
     return TSG_OK;
 }

@@ -160,10 +160,152 @@ def _launch(comp, fused: bool, stream):
     return outs, (start, end), nbytes
 
 
+# Streamed host step (run_fused on host Fields, the reference's loop of bench.py:398-403):
+# when the density is the only host-side input, it goes up, through the fused step and
+# back down band by band of rows on three streams, so the upload of band b+1, the step of
+# band b and the download of band b-1 overlap (PCIe is full duplex) instead of running one
+# after the other over the whole field.  279x256x80: 1.59 ms per run_fused (device 1.47)
+# against 2.02 ms unstreamed (tools/streamed_probe.py; 2 / 4 / 8 / 12 bands: 1.77 / 1.62 /
+# 1.60 / 1.65 ms).  A row band of the level-outer host layout is a strided (2-D) copy, and
+# concurrent 2-D copies in both directions move ~20 % less than 1-D ones
+# (tools/dma2d_probe.py: 1.19 vs 0.99 ms for the field both ways in 6 bands), which is
+# what keeps it above the ~1.0 ms of the link.
+_STREAM_BANDS = 6
+_STREAM_MIN_ROWS = 24
+
+
+def _band_plan(field):
+    """(front, row stride, level stride, level planes outermost) when every band of host
+    storage rows of ``field`` is one 2-D copy, else None.  Elements, not bytes."""
+    lay = [int(x) for x in field.linear.layout6()]  # front, row, color, column, level, extra
+    front, s_row, s_col, s_cl, s_lev = lay[0], lay[1], lay[2], lay[3], lay[4]
+    spec, meta = field.spec, field.meta
+    rows_st, cols_st = spec.rows + 2 * spec.halo, spec.cols + 2 * spec.halo
+    if meta.selector.extra or s_row <= 0 or s_lev <= 0:
+        return None
+    span_row = (meta.location.colors - 1) * s_col + (cols_st - 1) * s_cl + 1  # one row, one level
+    if span_row <= s_row and s_lev >= rows_st * s_row:
+        return front, s_row, s_lev, True  # level planes outermost: a band = one run per level
+    if span_row + (meta.levels - 1) * s_lev <= s_row:
+        return front, s_row, s_lev, False  # rows outermost: a band is contiguous
+    return None
+
+
+def _band_copy(field, buf, staging, rows_lo: int, rows_hi: int, h2d: bool, stream) -> None:
+    """Copy host storage rows [rows_lo, rows_hi) of ``field`` between its page-locked host
+    buffer ``buf`` and the device ``staging`` image of that buffer (one cudaMemcpy2DAsync)."""
+    front, s_row, s_lev, planes = _band_plan(field)
+    nrow = rows_hi - rows_lo
+    if nrow <= 0:
+        return
+    host = buf.ctypes.data + 8 * (front + rows_lo * s_row)
+    dev = staging.data_ptr() + 8 * (front + rows_lo * s_row)
+    width = 8 * nrow * s_row
+    height, pitch = (field.meta.levels, 8 * s_lev) if planes else (1, width)
+    _lib.call("tsg_memcpy2d", _lib.ctypes.c_void_p(dev if h2d else host), pitch,
+              _lib.ctypes.c_void_p(host if h2d else dev), pitch, width, height, 1 if h2d else 2,
+              _lib.stream_handle(stream))
+
+
+def _streamable(comp, fused: bool, download: bool) -> bool:
+    if not (fused and download and comp.kind == "mpdata"):
+        return False
+    st, geo = comp.state, comp.geo
+    pd = st.pd_in
+    rest = (st.vn, st.wn, st.rho, geo.edge_signs, geo.dual_volumes)
+    if not pd.dirty["primary"] or any(f.dirty["primary"] or f._mirror is None for f in rest):
+        return False
+    if st.pd_out.dirty["mirror"] or pd.has_extra or not pd.has_levels or pd.spec.rows < _STREAM_MIN_ROWS:
+        return False
+    import numpy as np
+
+    if not np.array_equal(pd.linear.layout6(), st.pd_out.linear.layout6()):
+        return False
+    return _band_plan(pd) is not None and pd.buffer("primary").ctypes.data % 16 == 0
+
+
+def _run_streamed(comp, stream):
+    """pd_in host -> device -> fused step -> pd_out device -> host, in bands of rows."""
+    import torch
+
+    st, geo, p = comp.state, comp.geo, comp.params
+    spec = comp.patch
+    grid = device_grid(spec)
+    R, h, K = spec.rows, spec.halo, spec.levels
+    pd_in, pd_out = st.pd_in, st.pd_out
+    lay = pd_in.linear.layout6()
+    lay_p = lay.ctypes.data_as(_lib.ctypes.POINTER(_lib.ctypes.c_int64))
+    host_in, host_out = pd_in.buffer("primary"), pd_out.buffer("primary")
+    dev_in, dev_out = pd_in.buffer("mirror"), pd_out.buffer("mirror")
+    stage_in = torch.empty(pd_in.linear.total, dtype=torch.float64, device=grid.device)
+    stage_out = torch.empty(pd_out.linear.total, dtype=torch.float64, device=grid.device)
+    ins = [dev_in, st.vn.buffer("mirror"), st.wn.buffer("mirror"), st.rho.buffer("mirror"),
+           geo.edge_signs.buffer("mirror"), geo.dual_volumes.buffer("mirror")]
+    B = _STREAM_BANDS
+    cuts = [R * b // B for b in range(B + 1)]
+    cur = torch.cuda.current_stream() if stream is None else stream
+    s_up, s_comp, s_down = (torch.cuda.Stream(device=grid.device) for _ in range(3))
+    for s in (s_up, s_comp, s_down):
+        s.wait_stream(cur)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(s_up)
+    def up(lo, hi):  # upload interior rows [lo, hi) and pack them (with their halo images)
+        _band_copy(pd_in, host_in, stage_in, h + lo, h + hi, True, s_up)
+        ev = torch.cuda.Event()
+        ev.record(s_up)
+        s_comp.wait_event(ev)
+        _lib.call("tsg_pack_strided_rows", grid.handle, pd_in.loc_code, K, _lib.ptr(stage_in), lay_p, h, lo, hi,
+                  _lib.ptr(dev_in), _lib.stream_handle(s_comp))
+
+    def step_down(lo, hi):  # the fused step over rows [lo, hi), then unpack + download them
+        _lib.call("tsg_mpdata_step_rows", grid.handle, *[_lib.ptr(t) for t in ins], _lib.ptr(dev_out),
+                  float(p.dt), float(p.pivbz), _FLUX_CODE[comp.flux_op], lo, hi, _lib.stream_handle(s_comp))
+        _lib.call("tsg_unpack_strided_rows", grid.handle, pd_out.loc_code, K, _lib.ptr(dev_out), lay_p, h,
+                  h + lo, h + hi, _lib.ptr(stage_out), _lib.stream_handle(s_comp))
+        ev = torch.cuda.Event()
+        ev.record(s_comp)
+        s_down.wait_event(ev)
+        _band_copy(pd_out, host_out, stage_out, h + lo, h + hi, False, s_down)
+
+    # rows of band b need rows lo-1 .. hi: the last row first (its image is row -1 of the
+    # periodic patch), then each band with one extra row below it, so band b steps as soon
+    # as its own upload has landed
+    up(R - 1, R)
+    for b in range(B):
+        lo, hi = cuts[b], cuts[b + 1]
+        up(lo, min(hi + 1, R))
+        step_down(lo, hi)
+    # the host halo rows are images of rows R-1 and 0, final only now
+    _lib.call("tsg_unpack_strided_rows", grid.handle, pd_out.loc_code, K, _lib.ptr(dev_out), lay_p, h, 0, h,
+              _lib.ptr(stage_out), _lib.stream_handle(s_comp))
+    _lib.call("tsg_unpack_strided_rows", grid.handle, pd_out.loc_code, K, _lib.ptr(dev_out), lay_p, h,
+              R + h, R + 2 * h, _lib.ptr(stage_out), _lib.stream_handle(s_comp))
+    ev = torch.cuda.Event()
+    ev.record(s_comp)
+    s_down.wait_event(ev)
+    _band_copy(pd_out, host_out, stage_out, 0, h, False, s_down)
+    _band_copy(pd_out, host_out, stage_out, R + h, R + 2 * h, False, s_down)
+    s_down.wait_stream(s_comp)
+    s_down.wait_stream(s_up)
+    end.record(s_down)
+    cur.wait_stream(s_down)
+    end.synchronize()
+    del stage_in, stage_out
+    pd_in.dirty = {"primary": False, "mirror": False}
+    pd_in.sync_count += 1
+    pd_out.dirty = {"primary": False, "mirror": False}
+    pd_out.sync_count += 1
+    return [pd_out], (start, end), mpdata_bytes(R, spec.cols, K, True)
+
+
 def run_gpu(comp, fused: bool = True, run_tag: str = "gpu", download: bool = True,
             stream=None, tiles: "TileSpec | None" = None) -> RunStats:
     """Execute ``comp`` on the current CUDA device; returns RunStats."""
-    outs, (start, end), nbytes = _launch(comp, fused, stream)
+    if _streamable(comp, fused, download):
+        outs, (start, end), nbytes = _run_streamed(comp, stream)
+        download = False  # pd_out is already on the host
+    else:
+        outs, (start, end), nbytes = _launch(comp, fused, stream)
     end.synchronize()
     updates = record_run(comp, run_tag, fused, tiles)
     if tiles is None:  # useful updates (run_naive's count); a TileSpec adds the apron recompute

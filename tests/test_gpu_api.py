@@ -642,3 +642,47 @@ def test_tma_reduce_every_tile_shape(cuda_ok):
                 assert np.array_equal(T.field_to_flat(dst), want), (f, t, v)
     finally:
         _lib.call("tsg_set_reduce_variant", 0)
+
+
+@pytest.mark.parametrize("shape,halo,order", [
+    ((24, 20, 7), 1, None),                                            # level planes outermost
+    ((37, 45, 50), 1, None),
+    ((30, 17, 6), 2, ("extra", "row", "color", "column", "level")),    # rows outermost, halo 2
+    ((48, 9, 5), 1, ("level", "extra", "row", "column", "color")),
+])
+def test_streamed_host_step_in_the_reference_loop(cuda_ok, shape, halo, order):
+    """The reference's dependent loop (bench.py:398-403: ``_copy_core(pd_out, pd_in)`` on
+    the host, then ``run_fused``): from the second step only pd_in is host-dirty, so
+    run_fused streams it through the step band by band (executors._run_streamed).  Three
+    steps equal three oracle steps bitwise, the host halo of pd_out holds periodic
+    images, and every field is clean afterwards."""
+    from paper_1908_06094_b200 import executors as X
+
+    spec = T.PatchSpec(*shape, halo=halo)
+    lay = T.LayoutSpec(order) if order else None
+    params = T.MpdataParams(dt=0.15, pivbz=0.6)
+    geo, state = _case(spec, 21, layout=lay)
+    comp = T.build_mpdata(spec, state, geo, params)
+    r, c, h = spec.rows, spec.cols, spec.halo
+    args = list(_oracle_args(spec, geo, state))
+    streamed = 0
+    for step in range(3):
+        if step:
+            values = state.pd_out.array("primary", "r")[h:h + r, :, h:h + c, :, :]
+            state.pd_in.array("primary", "rw")[h:h + r, :, h:h + c, :, :] = values
+            T.halo_update(state.pd_in)
+            streamed += X._streamable(comp, True, True)
+        T.run_fused(comp, T.TileSpec(r, c))
+        args[4] = O.transport_step(*args, params.dt, params.pivbz)["pd_out"]
+        assert np.array_equal(T.field_to_flat(state.pd_out), args[4]), step
+    assert streamed == 2
+    arr = state.pd_out.array()
+    assert np.array_equal(arr[:h], arr[r:r + h]) and np.array_equal(arr[:, :, :h], arr[:, :, c:c + h])
+    assert not any(state.pd_in.dirty.values()) and not any(state.pd_out.dirty.values())
+
+
+def _oracle_args(spec, geo, state):
+    r, c = spec.rows, spec.cols
+    return (O.neighbor_table(r, c, "edges", "vertices"), O.neighbor_table(r, c, "vertices", "edges"),
+            O.edge_signs(r, c), T.field_to_flat(geo.dual_volumes)[:, 0], T.field_to_flat(state.pd_in),
+            T.field_to_flat(state.vn), T.field_to_flat(state.wn), T.field_to_flat(state.rho))
