@@ -1,1 +1,1 @@
-timeout 300 python tools/dma2d_probe.py
+timeout 300 python tools/e2e_loop_breakdown.py 20
