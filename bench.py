@@ -561,7 +561,7 @@ def run_ours(args):
         del stepper
         torch.cuda.empty_cache()
 
-        host_fed = args.workload == "cfg3" and world == 1
+        host_fed = args.workload == "cfg3"  # e2e at every N; the other host-fed records at N = 1
         e2e = e2e_all = loop = e2e_loop = None
         if host_fed:
             V = my_rows * cols
@@ -585,12 +585,18 @@ def run_ours(args):
             def e2e_run(step_inputs, api):
                 st.run_pipelined([pinned] * 3, outs + outs[:1], DT, PIVBZ)  # warm-up (all inputs)
                 torch.cuda.synchronize()
+                barrier()
                 e0, e1 = st.run_pipelined([step_inputs] * e2e_steps,
                                           [outs[n % 2] for n in range(e2e_steps)], DT, PIVBZ)
                 torch.cuda.synchronize()
-                t_e2e = e0.elapsed_time(e1) / 1e3 / e2e_steps
+                barrier()
+                t_e2e = _max_over_ranks(e0.elapsed_time(e1) / 1e3 / e2e_steps, world, shared)
                 h2d = sum(t.numel() * 8 for t in step_inputs if t is not None)
-                return {"value": V * K / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                if world > 1:
+                    api += (f"; at N = {world} every rank feeds its own 279x256x80 periodic patch from its "
+                            "host (the weak-scaling per-GPU work; the strips' halo exchange is not on "
+                            "the host-fed path), value = N x V K / the slowest rank's time, bytes per rank")
+                return {"value": world * V * K / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3,
                         "pcie_gbs": (h2d + d2h) / t_e2e / 1e9, "api": api}
 
@@ -600,30 +606,35 @@ def run_ours(args):
                           "step, reorder, D2H of pd_out; vn / wn / rho resident (fixed, as in the "
                           "reference's loop); steps overlapped (H2D n+1 | GPU n | D2H n-1) since they "
                           "do not depend on each other -- see e2e_time_loop for the dependent loop")
-            e2e_all = e2e_run(pinned, "independent host-fed steps as e2e, with every input (pd / vn / "
-                                      "wn / rho, the flat oracle call of reference.py:93-116) copied "
-                                      "H2D per step")
-            # the same dependent loop with the static schedule (per-step launches replayed as a
-            # captured two-step graph, round 1's loop) for comparison
-            n_loop = args.steps
-            _lib.call("tsg_set_fused_schedule", 1)
-            try:
-                st.run(n_loop, DT, PIVBZ)
-                flush_l2()
-                torch.cuda.synchronize()
-                t_loop = _timed_run(st, n_loop, stream) / n_loop
-            finally:
-                _lib.call("tsg_set_fused_schedule", 0)
-            loop = {"value": V * K / t_loop, "unit": UNIT, "ms_per_step": t_loop * 1e3, "steps": n_loop,
-                    "roofline_frac": mpdata_algorithmic_bytes(w["rows"], cols, K) / t_loop / 1e9 / peak,
-                    "api": "StructuredStepper.run with tsg_set_fused_schedule(1): static per-CTA ranges, "
-                           "one launch per step replayed as a captured two-step CUDA graph"}
-            del st
-            torch.cuda.empty_cache()
-            try:  # informational beside e2e: never lose the line over it
-                e2e_loop = e2e_time_loop(w, max(5, min(args.steps, 20)))
-            except Exception as exc:  # noqa: BLE001
-                e2e_loop = {"unavailable": f"{type(exc).__name__}: {exc}"}
+            if world == 1:
+                e2e_all = e2e_run(pinned, "independent host-fed steps as e2e, with every input (pd / vn / "
+                                          "wn / rho, the flat oracle call of reference.py:93-116) copied "
+                                          "H2D per step")
+            if world == 1:
+                # the same dependent loop with the static schedule (per-step launches replayed as a
+                # captured two-step graph, round 1's loop) for comparison
+                n_loop = args.steps
+                _lib.call("tsg_set_fused_schedule", 1)
+                try:
+                    st.run(n_loop, DT, PIVBZ)
+                    flush_l2()
+                    torch.cuda.synchronize()
+                    t_loop = _timed_run(st, n_loop, stream) / n_loop
+                finally:
+                    _lib.call("tsg_set_fused_schedule", 0)
+                loop = {"value": V * K / t_loop, "unit": UNIT, "ms_per_step": t_loop * 1e3, "steps": n_loop,
+                        "roofline_frac": mpdata_algorithmic_bytes(w["rows"], cols, K) / t_loop / 1e9 / peak,
+                        "api": "StructuredStepper.run with tsg_set_fused_schedule(1): static per-CTA ranges, "
+                               "one launch per step replayed as a captured two-step CUDA graph"}
+                del st
+                torch.cuda.empty_cache()
+                try:  # informational beside e2e: never lose the line over it
+                    e2e_loop = e2e_time_loop(w, max(5, min(args.steps, 20)))
+                except Exception as exc:  # noqa: BLE001
+                    e2e_loop = {"unavailable": f"{type(exc).__name__}: {exc}"}
+            else:
+                del st
+                torch.cuda.empty_cache()
         o1280 = None
         if args.workload == "cfg3" and not args.no_o1280:
             o1280 = o1280_strong(args, rank, world, shared, barrier, peak)
