@@ -136,3 +136,20 @@ def test_strip_stepper_run_on_one_gpu_is_the_persistent_loop(cuda_ok):
             b.swap()
         assert np.array_equal(a.interior("pd").cpu().numpy(), b.interior("pd").cpu().numpy())
         assert a.steps_done == b.steps_done == n
+
+
+def test_long_persistent_loops_match_single_steps(cuda_ok):
+    """A 501-step launch, then a second one of 250 steps on the same handle (the tile
+    counters' base carried across launches), equals 751 single launches bitwise."""
+    shape = (37, 45, 50)
+    inp, st = _stepper(shape, 9)
+    st.run(501, 0.1, 1.0)
+    st.swap()
+    st.run(250, 0.1, 1.0)
+    a = st.download()
+    assert _wait_error(st) == 0
+    inp2, st2 = _stepper(shape, 9)
+    for _ in range(751):
+        st2.step(0.1, 1.0)
+        st2.swap()
+    assert np.array_equal(a, st2.fetch("pd"))

@@ -1,5 +1,1 @@
-OLD=$PWD/paper_1908_06094_b200/libtsg_old.so
-for i in 1 2; do
-echo new; timeout 300 python tools/celldiv_probe.py
-echo old; TSG_LIBRARY=$OLD timeout 300 python tools/celldiv_probe.py
-done
+timeout 900 python -m pytest tests/test_gpu_schedule.py -q -x 2>&1 | tail -3
