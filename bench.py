@@ -508,6 +508,8 @@ def run_ours(args):
         # every rank steps its strip through the same path at every N; the cfg3 strips carry
         # the reference's _transport_setup fields of one 279x256x80 patch each
         stepper = StripStepper(global_rows, cols, K, rank, world, seed=0, mode=args.exchange)
+        if world > 1 and stepper.mode != args.exchange:  # peer mapping failed on some rank
+            args.exchange, exchange_note = stepper.mode, stepper.fallback
         my_rows = stepper.nrows
         inp = None
         if args.workload == "cfg3":
@@ -666,8 +668,9 @@ def run_ours(args):
                   "path": "StripStepper" + (" (periodic patch)" if world == 1 else f" ({args.exchange})"),
                   "parallelism": f"row-strips x{world}",
                   "halo_exchange": ("none" if world == 1 else
-                                    "one launch per step: boundary-row epilogue stores into the "
-                                    "neighbours' halos (CUDA IPC over NVLink), in-kernel step fence"
+                                    "inside the persistent loop launch: boundary-row epilogue stores "
+                                    "into the neighbours' halos (CUDA IPC over NVLink), per-step "
+                                    "neighbour flags acquired / released in the kernel"
                                     if args.exchange == "p2p" else "NCCL grouped send/recv"),
                   **({"exchange_fallback": exchange_note} if exchange_note else {}),
                   "l2": "no flush between the timed loop's steps (each streams 320 MB per rank through "

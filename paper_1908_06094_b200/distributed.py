@@ -214,6 +214,7 @@ class StripStepper:
         if mode not in ("nccl", "p2p"):
             raise ValueError(f"exchange mode must be 'nccl' or 'p2p', got {mode!r}")
         self.mode = mode if world > 1 else "nccl"
+        self.fallback = ""  # why a requested p2p exchange runs as NCCL send / recv
         self.timeout_ms = timeout_ms
         # p2p: the whole step in one launch (default) or the five-launch sequence
         # (interior rows, fence, two boundary-row launches, signal)
@@ -248,10 +249,24 @@ class StripStepper:
         every = [None] * self.world
         dist.all_gather_object(every, mine, group=self.group)
         self._peers = {}
-        for r in {self.strips.up(self.rank), self.strips.down(self.rank)}:
-            h0, h1, hf, nr = every[r]
-            bufs = [RawBuffer.open(h) for h in (h0, h1)]
-            self._peers[r] = dict(bufs=bufs, flags=RawBuffer.open(hf), nrows=nr)
+        why = ""
+        try:
+            for r in {self.strips.up(self.rank), self.strips.down(self.rank)}:
+                h0, h1, hf, nr = every[r]
+                bufs = [RawBuffer.open(h) for h in (h0, h1)]
+                self._peers[r] = dict(bufs=bufs, flags=RawBuffer.open(hf), nrows=nr)
+        except Exception as exc:  # noqa: BLE001 -- any rank's failure moves every rank to NCCL
+            why = f"rank {self.rank}: {type(exc).__name__}: {exc}"
+        verdicts = [None] * self.world
+        dist.all_gather_object(verdicts, why, group=self.group)
+        failed = [v for v in verdicts if v]
+        if failed:  # consistent fallback: the NCCL (or gloo) send / recv exchange
+            self._peers = {}
+            self.mode = "nccl"
+            self.fallback = "peer mapping failed (" + failed[0] + "): NCCL exchange"
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)
+            return
         self._rowstride = self.pd.stride(0) * 8  # bytes per storage row
         self._parity = 0  # pd = raw[parity], pd_out = raw[1 - parity]
         torch.cuda.synchronize()
