@@ -86,7 +86,9 @@ def _peaks():
 def workload_config(w: dict, world: int) -> dict:
     """The ``config`` both arms print for one workload at N ranks (identical dicts)."""
     rows = w["rows"] * world if w["scaling"] == "weak" else w["rows"]
-    return {"workload": w["label"], "rows": rows, "cols": w["cols"], "levels": w["levels"]}
+    return {"workload": w["label"], "rows": rows, "cols": w["cols"], "levels": w["levels"],
+            "l2": "inputs larger than L2: every step streams the whole state (>= 320 MB per GPU) "
+                  "through the 126 MB L2; one 256 MiB L2 flush before the timed region"}
 
 
 def step_stats(ms: list) -> dict:
