@@ -253,6 +253,8 @@ def _p2p_worker(rank, world, port, q, single_launch=True, graph=False, shape=(17
     (2, True, False, (17, 29, 18)), (2, False, False, (17, 29, 18)), (3, True, False, (17, 29, 18)),
     (2, True, True, (17, 29, 18)), (3, True, True, (17, 29, 18)), (2, True, "mixed", (17, 29, 18)),
     (2, True, True, (9, 40, 80)),
+    # four ranks, uneven strips (6 / 6 / 6 / 5 rows: tile rows cut by strip edges)
+    (4, True, True, (23, 29, 18)),
     # strips large enough for the band schedule (interior rows banded, boundary rows last)
     (2, True, True, (512, 608, 32))])
 def test_p2p_fused_exchange_processes_share_one_gpu(cuda_ok, world, single_launch, graph, shape):
