@@ -556,6 +556,20 @@ def run_ours(args):
             stepper.finish()
             stepper.check()
         flushed_s = _max_over_ranks(sum(step_ms) / 1e3, world, shared) / len(step_ms)
+        sustained = None
+        if world == 1 and args.sustained_seconds > 0:
+            # the same loop kept busy for a few seconds: what it settles to under the power cap
+            t_end, last = time.perf_counter() + args.sustained_seconds, []
+            while time.perf_counter() < t_end:
+                last.append(_timed_run(stepper, 200, stream) / 200)
+            tail = last[len(last) // 2:]
+            t_sus = statistics.median(tail)
+            sustained = {"ms_per_step": t_sus * 1e3, "value": GV * K / t_sus,
+                         "roofline_frac": mpdata_algorithmic_bytes(my_rows, cols, K) / t_sus / 1e9 / peak,
+                         "sm_mhz_after": _sm_clock_mhz(local),
+                         "how": f"back-to-back 200-step launches for {args.sustained_seconds:g} s, "
+                                "median of the second half (the headline is taken within the first "
+                                "~0.1 s of GPU work, at boost clock)"}
         variant = _lib.lib().tsg_fused_variant_of(stepper.grid.handle, 0, my_rows)
         band = world == 1 and _lib.lib().tsg_fused_band_of(stepper.grid.handle, 0, my_rows) == 1
         hits = _lib.ctypes.c_int64()
@@ -706,6 +720,7 @@ def run_ours(args):
         "e2e_time_loop": e2e_loop,
         "time_loop": loop,
         "o1280_strong": o1280,
+        "sustained": sustained,
         "gpu_launches": loop_launches,
         "clocks": clocks.summary(),
         "timed_wall_s": t_wall,
@@ -734,6 +749,8 @@ def main(argv=None):
                     help="timed steps of the o1280_strong record (cfg3 runs)")
     ap.add_argument("--no-o1280", action="store_true", help="skip the o1280_strong record")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--sustained-seconds", type=float, default=3.0,
+                    help="N = 1: also run the headline loop back to back this long (0: skip)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-python-ref", action="store_true",
                     help="reference arm: skip timing the reference package itself")

@@ -1,1 +1,1 @@
-timeout 600 python tools/loop_paths_probe.py
+timeout 600 python tools/sustained_variants.py 3
