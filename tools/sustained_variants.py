@@ -38,6 +38,8 @@ def loop(op_name):
 forms = [("persistent loop, upwind", loop("upwind")), ("persistent loop, centred", loop("centred")),
          ("single launches, upwind", single(0)), ("single launches, data probe (op 99)", single(99)),
          ("single launches, compute probe (op 98)", single(98))]
+if len(sys.argv) > 2:  # a subset by index, e.g. 0,1
+    forms = [forms[int(q)] for q in sys.argv[2].split(",")]
 for name, fn in forms:
     fn()
     torch.cuda.synchronize()
