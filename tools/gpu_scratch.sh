@@ -1,1 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_bench_contract.py -q -x 2>&1 | tail -5
+timeout 900 python bench.py > gpurun_out/bench_s.log 2>&1
+python tools/bench_brief.py gpurun_out/bench_s.log
+timeout 900 python bench.py > gpurun_out/bench_s2.log 2>&1
+python tools/bench_brief.py gpurun_out/bench_s2.log
