@@ -1,4 +1,6 @@
-timeout 900 python bench.py > gpurun_out/bench_s.log 2>&1
-python tools/bench_brief.py gpurun_out/bench_s.log
-timeout 900 python bench.py > gpurun_out/bench_s2.log 2>&1
-python tools/bench_brief.py gpurun_out/bench_s2.log
+timeout 900 python -m pytest tests/test_gpu_api.py tests/test_gpu_parity.py tests/test_gpu_acceptance.py -q -x 2>&1 | tail -2
+timeout 900 python tools/bench_stencils.py r2e > /dev/null 2>&1; python -c "
+import json
+for d in json.load(open('gpurun_out/stencils_r2e.json')):
+    if d['name'].startswith('mpdata'): print(d['name'], d['patch'], round(d['us'],1), round(d['frac'],3), d.get('fused_speedup'))
+"
