@@ -4,6 +4,7 @@ power cap, or only the SM clock?  python tools/sustained_copy_probe.py [S]"""
 import sys
 import time
 
+import pynvml
 import torch
 
 S = float(sys.argv[1]) if len(sys.argv) > 1 else 4.0
@@ -14,6 +15,8 @@ for _ in range(3):
     b.copy_(a)
 torch.cuda.synchronize()
 time.sleep(1.0)
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(0)
 t0 = time.perf_counter()
 rows = []
 while time.perf_counter() - t0 < S:
@@ -23,6 +26,7 @@ while time.perf_counter() - t0 < S:
         b.copy_(a)
     e1.record()
     e1.synchronize()
-    rows.append((time.perf_counter() - t0, 50 * 2 * n * 8 / (e0.elapsed_time(e1) / 1e3) / 1e9))
+    rows.append((time.perf_counter() - t0, 50 * 2 * n * 8 / (e0.elapsed_time(e1) / 1e3) / 1e9,
+                 pynvml.nvmlDeviceGetPowerUsage(h) / 1e3))
 for k in range(0, len(rows), max(1, len(rows) // 20)):
-    print(f"t={rows[k][0]:6.3f}s  {rows[k][1]:7.1f} GB/s")
+    print(f"t={rows[k][0]:6.3f}s  {rows[k][1]:7.1f} GB/s  {rows[k][2]:6.0f} W")

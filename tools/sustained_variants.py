@@ -6,6 +6,8 @@ import statistics
 import sys
 import time
 
+import pynvml
+
 sys.path.insert(0, "/root/repo")
 import torch  # noqa: E402
 
@@ -40,11 +42,13 @@ forms = [("persistent loop, upwind", loop("upwind")), ("persistent loop, centred
          ("single launches, compute probe (op 98)", single(98))]
 if len(sys.argv) > 2:  # a subset by index, e.g. 0,1
     forms = [forms[int(q)] for q in sys.argv[2].split(",")]
+pynvml.nvmlInit()
+_h = pynvml.nvmlDeviceGetHandleByIndex(0)
 for name, fn in forms:
     fn()
     torch.cuda.synchronize()
     time.sleep(2.0)  # cool down
-    t0, ts = time.perf_counter(), []
+    t0, ts, watts, clk = time.perf_counter(), [], [], []
     while time.perf_counter() - t0 < S:
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
@@ -52,6 +56,9 @@ for name, fn in forms:
         b.record()
         b.synchronize()
         ts.append(a.elapsed_time(b) * 1e3 / 200)
+        watts.append(pynvml.nvmlDeviceGetPowerUsage(_h) / 1e3)
+        clk.append(pynvml.nvmlDeviceGetClockInfo(_h, pynvml.NVML_CLOCK_SM))
     settled = statistics.median(ts[len(ts) // 2:])
-    print(f"{name:40s} first {ts[0]:6.2f} us, settled {settled:6.2f} us/step ({B / settled / 1e3 / 6455:.3f})",
-          flush=True)
+    w, c = statistics.median(watts[len(watts) // 2:]), statistics.median(clk[len(clk) // 2:])
+    print(f"{name:40s} first {ts[0]:6.2f} us, settled {settled:6.2f} us/step ({B / settled / 1e3 / 6455:.3f}) "
+          f"at {w:.0f} W, {c} MHz", flush=True)
