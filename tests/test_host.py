@@ -70,6 +70,27 @@ def test_argument_errors_map_to_reference_exceptions():
     with pytest.raises(ValueError, match="variant"):
         _lib.check(lib.tsg_set_fused_variant(99))
     assert "variant" in lib.tsg_last_error().decode()
+    # round-2 entry points validate before any device work
+    with pytest.raises(ValueError, match="reduce variant"):
+        _lib.check(lib.tsg_set_reduce_variant(20))
+    with pytest.raises(ValueError, match="NULL"):
+        _lib.check(lib.tsg_flat_flux(None, p, p, 4, 2, 0, p, None))
+    with pytest.raises(ValueError, match="operator"):
+        _lib.check(lib.tsg_flat_flux(p, p, p, 4, 2, 5, p, None))
+    with pytest.raises(ValueError, match="at least 2 levels"):
+        _lib.check(lib.tsg_flat_fluz(p, p, 4, 1, 1.0, p, None))
+    with pytest.raises(ValueError, match="bad shape"):
+        _lib.check(lib.tsg_flat_divergence(p, -1, p, p, p, p, 4, 2, p, None))
+    with pytest.raises(ValueError, match="NULL"):
+        _lib.check(lib.tsg_flat_advance(p, None, p, 4, 0.1, p, None))
+    with pytest.raises(ValueError, match="bad shape"):
+        _lib.check(lib.tsg_flat_cell_divergence(p, 3, p, p, p, 4, 0, p, None))
+    with pytest.raises(ValueError, match="kind"):
+        _lib.check(lib.tsg_memcpy2d(p, 64, p, 64, 64, 2, 3, None))
+    with pytest.raises(ValueError, match="extents"):
+        _lib.check(lib.tsg_memcpy2d(p, 32, p, 64, 64, 2, 1, None))
+    with pytest.raises(ValueError, match="grid is NULL"):
+        _lib.check(lib.tsg_pack_strided_rows(None, 0, 4, p, None, 1, 0, 1, p, None))
 
 
 def test_grid_create_validates_before_touching_the_device():
