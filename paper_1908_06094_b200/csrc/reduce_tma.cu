@@ -140,7 +140,11 @@ __global__ void __launch_bounds__(C::kThreads)
                 d_live = false;
                 info[stage] = make_int2(-1, 0);
                 mbar_arrive(bar);
+                // order this CTA's ticket takes before its done count: the CTA that resets
+                // the words must see every take (else a stale count leaks into the next launch)
+                __threadfence();
                 if (atomicAdd(&a.ticket[1], 1u) == gridDim.x - 1) {  // every CTA is done taking
+                    __threadfence();
                     a.ticket[0] = 0;
                     a.ticket[1] = 0;
                 }

@@ -686,3 +686,25 @@ def _oracle_args(spec, geo, state):
     return (O.neighbor_table(r, c, "edges", "vertices"), O.neighbor_table(r, c, "vertices", "edges"),
             O.edge_signs(r, c), T.field_to_flat(geo.dual_volumes)[:, 0], T.field_to_flat(state.pd_in),
             T.field_to_flat(state.vn), T.field_to_flat(state.wn), T.field_to_flat(state.rho))
+
+
+def test_dealt_reduce_many_launches_stay_exact(cuda_ok):
+    """The dealt reduce's ticket words reset themselves at the end of every launch: 200
+    back-to-back launches on one handle (no host sync in between) each give the same
+    bitwise result -- a count leaking into the next launch would skip work."""
+    import torch
+
+    from paper_1908_06094_b200 import _lib
+    from paper_1908_06094_b200.device import DeviceGrid
+
+    g = DeviceGrid(512, 512, 33)
+    s = _lib.stream_handle()
+    src, ref, dst = g.empty(0, 33), g.empty(0, 33), g.empty(0, 33)
+    _lib.call("tsg_fill_hash", g.handle, 0, 33, 3, 0.0, 1.0, _lib.ptr(src), s)
+    _lib.call("tsg_neighbor_reduce", g.handle, 0, 0, 33, _lib.ptr(src), None, _lib.ptr(ref), s)
+    bad = torch.zeros((), dtype=torch.int64, device="cuda")
+    for _ in range(200):
+        dst.zero_()
+        _lib.call("tsg_neighbor_reduce", g.handle, 0, 0, 33, _lib.ptr(src), None, _lib.ptr(dst), s)
+        bad += (dst != ref).any()
+    assert int(bad) == 0
