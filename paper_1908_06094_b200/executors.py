@@ -224,6 +224,19 @@ def _streamable(comp, fused: bool, download: bool) -> bool:
     return _band_plan(pd) is not None and pd.buffer("primary").ctypes.data % 16 == 0
 
 
+_STREAMS = {}
+
+
+def _stream_set(device):
+    """Three side streams per device for the streamed host step (created once)."""
+    import torch
+
+    key = str(device)
+    if key not in _STREAMS:
+        _STREAMS[key] = tuple(torch.cuda.Stream(device=device) for _ in range(3))
+    return _STREAMS[key]
+
+
 def _run_streamed(comp, stream):
     """pd_in host -> device -> fused step -> pd_out device -> host, in bands of rows."""
     import torch
@@ -244,7 +257,7 @@ def _run_streamed(comp, stream):
     B = _STREAM_BANDS
     cuts = [R * b // B for b in range(B + 1)]
     cur = torch.cuda.current_stream() if stream is None else stream
-    s_up, s_comp, s_down = (torch.cuda.Stream(device=grid.device) for _ in range(3))
+    s_up, s_comp, s_down = _stream_set(grid.device)
     for s in (s_up, s_comp, s_down):
         s.wait_stream(cur)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
