@@ -1,2 +1,8 @@
-timeout 900 python -m pytest tests/test_gpu_api.py -q -x -k "streamed" 2>&1 | tail -2
-timeout 300 python tools/streamed_probe.py 2>&1 | tail -3
+for d in 2 3 4 2 3; do
+TSG_PIPE_DEPTH=$d timeout 600 python bench.py --steps 100 --no-o1280 --no-cpu --sustained-seconds 0 > gpurun_out/bp.log 2>&1
+python -c "
+import json
+d=json.loads(open('gpurun_out/bp.log').read().strip().splitlines()[-1])
+print('depth $d', round(d['e2e']['ms_per_step'],4), round(d['e2e_all_inputs']['ms_per_step'],3))
+"
+done
