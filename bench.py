@@ -26,19 +26,25 @@ U[-0.5,0.5) velocities, rho = 1, uniform geometry, dt = 0.1, pivbz = 1).
 * o1280_strong: configs[4], the 2560 x 2576 x 137 patch cut into N strips
   through the same StripStepper path (on-device counter-hash inputs), for the
   strong-scaling efficiency T1 / (N * T_N) against the N = 1 run's record.
-* e2e (N = 1): independent host-fed steps through the flat-array API
+* e2e: independent host-fed steps through the flat-array API
   (StructuredStepper.run_pipelined): per step H2D of pd from pinned memory,
-  reorder, fused step, reorder, D2H of pd_out, overlapped across steps.
+  reorder, fused step, reorder, D2H of pd_out, overlapped across steps; at N > 1
+  every rank feeds its own 279 x 256 x 80 patch (max over ranks).  N = 1 only:
   ``e2e_all_inputs``: the same with every input (pd / vn / wn / rho) copied per
   step.  ``e2e_time_loop``: the reference's dependent loop (bench.py:398-403):
   ``_copy_core(pd_out, pd_in)`` on the host Fields, then ``run_fused(comp,
   TileSpec)`` -- no overlap possible, step n+1 consumes step n's output.
 * roofline: algorithmic bytes B_comp per step / average step time, against
   the measured HBM copy bandwidth (MEASURED_PEAKS.json).
+* sustained (N = 1, last, outside the clock sampling): the headline loop kept
+  busy for --sustained-seconds, the step time it settles to under the board's
+  power cap, with the board power and updates per joule.
 * cpu_baseline / --impl reference: the reference algorithm restated in C
   (oracle/c, bitwise equal to the reference, OpenMP over all host cores),
-  median step of the same sampling protocol in both arms; the reference arm also
-  times the reference package itself (``run_fused``, baseline/_ref) when installed.
+  median step of the same sampling protocol in both arms (the repo arm checks the
+  benchmarked kernel's result against the sample's own output, bitwise); the
+  reference arm also times the reference package itself (``run_fused``,
+  ``run_naive``, ``reference.transport_step``; baseline/_ref) when installed.
 """
 
 from __future__ import annotations

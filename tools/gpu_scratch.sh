@@ -1,8 +1,4 @@
-for d in 2 3 4 2 3; do
-TSG_PIPE_DEPTH=$d timeout 600 python bench.py --steps 100 --no-o1280 --no-cpu --sustained-seconds 0 > gpurun_out/bp.log 2>&1
-python -c "
-import json
-d=json.loads(open('gpurun_out/bp.log').read().strip().splitlines()[-1])
-print('depth $d', round(d['e2e']['ms_per_step'],4), round(d['e2e_all_inputs']['ms_per_step'],3))
-"
-done
+CS=/usr/local/cuda/bin/compute-sanitizer
+timeout 3300 $CS --tool memcheck --target-processes all --print-limit 5 python -m pytest tests -m gpu -q -x -k "not o1280 and not bench_line" > gpurun_out/memcheck_all_r2.log 2>&1
+echo rc=$?
+grep -v "^=========     \(#\|in \|Saved\)" gpurun_out/memcheck_all_r2.log | tail -6
