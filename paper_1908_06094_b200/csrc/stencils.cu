@@ -292,11 +292,24 @@ __global__ void __launch_bounds__(256) advance_kernel(FieldIx Fv, int K, double 
 // Level-pair item forms of the four unfused stages: one thread per
 // (element, level pair) over the whole field, kUnroll items per thread per pass, 16-byte
 // loads and stores -- the element-line forms above are latency-bound with a quarter of
-// their lanes idle in the last pass of an 80-level run.
-#define TSG_ITEMS(base, u, D)                                                                  \
-    for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x, T_ = gridDim.x * blockDim.x;   \
-         base < (D).n; base += kUnroll * T_)                                                     \
-        _Pragma("unroll") for (int u = 0; u < kUnroll; ++u)                                     \
+// their lanes idle in the last pass of an 80-level run.  Item order: on a resident grid
+// (item_grid, short sweeps) thread t's items of a pass are t, t + T, ... (T = all threads);
+// on a one-pass grid (long sweeps) the stencil stages take a block's kUnroll x 256 items
+// contiguously instead, so the items in flight form one wavefront rather than kUnroll
+// wavefronts a quarter of the field apart, and the row a stencil reads one row ahead is
+// still in L2 when its own items arrive: O1280 flux reads 31.6 vs 36.4 GB, divergence 31.4
+// vs 38.7 GB, the step 25.9 vs 27.1 ms (profiles/unfused_o1280_r2.csv).  On the resident
+// grid of a short sweep the strided order is faster (279x256x80: 170 vs 176 us).
+// 64-bit pass arithmetic: n may approach 2^32.
+#ifndef TSG_CHUNK_MASK  // A/B builds only: which stages take contiguous chunks on one pass
+#define TSG_CHUNK_MASK 7
+#endif
+#define TSG_ITEMS(base, u, D, BIT)                                                               \
+    const bool ch_ = (TSG_CHUNK_MASK & (BIT)) && (uint64_t)kUnroll * gridDim.x * blockDim.x >= (D).n; \
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * (ch_ ? kUnroll : 1) + threadIdx.x, \
+                  T_ = ch_ ? blockDim.x : (uint64_t)gridDim.x * blockDim.x;                      \
+         base < (D).n; base += (uint64_t)kUnroll * gridDim.x * blockDim.x)                       \
+        _Pragma("unroll") for (int u = 0; u < kUnroll; ++u)                                       \
             if (base + u * T_ < (D).n)
 
 // Edge fluxes of the unfused step (mpdata.py:189-199), three per vertex item: edge
@@ -310,8 +323,8 @@ __global__ void __launch_bounds__(256) flux3_pairs_kernel(FieldIx Fp, FieldIx Fe
                                                           const double *__restrict__ pd,
                                                           const double *__restrict__ vn,
                                                           double *__restrict__ flux, int flags) {
-    TSG_ITEMS(base, u, D) {
-        const Pt e = decompose(base + u * T_, D);
+    TSG_ITEMS(base, u, D, 1) {
+        const Pt e = decompose((uint32_t)(base + u * T_), D);
         const int k = 2 * e.k;
         const double2 po = ld2(pd + Fp.at(e.i, 0, e.j) + k);
         const double2 p0 = ld2(pd + Fp.at(e.i, 0, e.j + 1) + k);      // c0 (0,+1)
@@ -332,8 +345,8 @@ __global__ void __launch_bounds__(256) fluz_pairs_kernel(FieldIx Fp, FieldIx Fw,
                                                          double pivbz, const double *__restrict__ pd,
                                                          const double *__restrict__ wn,
                                                          double *__restrict__ fluz, int flags) {
-    TSG_ITEMS(base, u, D) {
-        const Pt e = decompose(base + u * T_, D);
+    TSG_ITEMS(base, u, D, 2) {
+        const Pt e = decompose((uint32_t)(base + u * T_), D);
         const double *P = pd + Fp.at(e.i, 0, e.j), *W = wn + Fw.at(e.i, 0, e.j);
         double f[2];
 #pragma unroll
@@ -356,8 +369,8 @@ __global__ void __launch_bounds__(256) div_pairs_kernel(FieldIx Fe, FieldIx Fw, 
                                                         const double *__restrict__ dual,
                                                         double *__restrict__ divvd, int flags) {
     constexpr int REL = TSG_VERTICES * 3 + TSG_EDGES;
-    TSG_ITEMS(base, u, D) {
-        const Pt e = decompose(base + u * T_, D);
+    TSG_ITEMS(base, u, D, 4) {
+        const Pt e = decompose((uint32_t)(base + u * T_), D);
         const int k = 2 * e.k;
         const double *S = signs + Fs.at(e.i, 0, e.j);
         const double *Z = fluz + Fw.at(e.i, 0, e.j);
@@ -385,8 +398,8 @@ __global__ void __launch_bounds__(256) advance_pairs_kernel(FieldIx Fv, PointDec
                                                             const double *__restrict__ divvd,
                                                             const double *__restrict__ rho,
                                                             double *__restrict__ pd_out, int flags) {
-    TSG_ITEMS(base, u, D) {
-        const Pt e = decompose(base + u * T_, D);
+    TSG_ITEMS(base, u, D, 8) {
+        const Pt e = decompose((uint32_t)(base + u * T_), D);
         const int64_t q = Fv.at(e.i, 0, e.j) + 2 * e.k;
         const double2 d = ld2(divvd + q), r = ld2(rho + q), p = ld2(pd + q);
         put2(pd_out + Fv.at(e.i, 0, e.j), images(Fv, e.i, e.j, flags), 2 * e.k,
@@ -757,16 +770,21 @@ extern "C" int tsg_mpdata_step_unfused(const tsg_grid *g, const double *pd, cons
         // an odd level count's last pair ends in the padding of every field (even pitch)
         const int np = (K + 1) / 2;
         const PointDec DV(g->rows, C, 1, np), DZ(g->rows, C, 1, K / 2 + 1);
-        auto blocks = [&](const PointDec &D) { return (unsigned)std::min<int64_t>(
-            (D.n + 256 * kUnroll - 1) / (256 * kUnroll), (int64_t)sms * 8); };
+        auto blocks = [&](const void *kernel, const PointDec &D) {
+            return item_grid(kernel, D.n, kUnroll, sms);
+        };
         if (flux_op == TSG_UPWIND)
-            flux3_pairs_kernel<TSG_UPWIND><<<blocks(DV), 256, 0, st>>>(Fv, Fe, DV, pd, vn, flux, g->flags);
+            flux3_pairs_kernel<TSG_UPWIND><<<blocks((const void *)flux3_pairs_kernel<TSG_UPWIND>, DV), 256, 0, st>>>(
+                Fv, Fe, DV, pd, vn, flux, g->flags);
         else
-            flux3_pairs_kernel<TSG_CENTRED><<<blocks(DV), 256, 0, st>>>(Fv, Fe, DV, pd, vn, flux, g->flags);
-        fluz_pairs_kernel<<<blocks(DZ), 256, 0, st>>>(Fv, Fw, DZ, K, pivbz, pd, wn, fluz, g->flags);
-        div_pairs_kernel<<<blocks(DV), 256, 0, st>>>(Fe, Fw, Fs, Fd, Fv, DV, flux, fluz, signs, dual, divvd,
-                                                     g->flags);
-        advance_pairs_kernel<<<blocks(DV), 256, 0, st>>>(Fv, DV, dt, pd, divvd, rho, pd_out, g->flags);
+            flux3_pairs_kernel<TSG_CENTRED><<<blocks((const void *)flux3_pairs_kernel<TSG_CENTRED>, DV), 256, 0, st>>>(
+                Fv, Fe, DV, pd, vn, flux, g->flags);
+        fluz_pairs_kernel<<<blocks((const void *)fluz_pairs_kernel, DZ), 256, 0, st>>>(Fv, Fw, DZ, K, pivbz, pd, wn,
+                                                                                       fluz, g->flags);
+        div_pairs_kernel<<<blocks((const void *)div_pairs_kernel, DV), 256, 0, st>>>(
+            Fe, Fw, Fs, Fd, Fv, DV, flux, fluz, signs, dual, divvd, g->flags);
+        advance_pairs_kernel<<<blocks((const void *)advance_pairs_kernel, DV), 256, 0, st>>>(Fv, DV, dt, pd, divvd,
+                                                                                             rho, pd_out, g->flags);
         TSG_CHECK_LAUNCH();
         return TSG_OK;
     }
@@ -799,14 +817,18 @@ extern "C" int tsg_transport_indirect(const int64_t *e2v, const int64_t *v2e, co
         a16(pd) && a16(vn) && a16(rho) && a16(flux) && a16(div) && a16(pd_out)) {
         const int np = nlev / 2;
         const uint32_t nE = (uint32_t)(ne * np), nV = (uint32_t)(nv * np), nZ = (uint32_t)(nv * (np + 1));
-        auto blocks = [&](uint32_t n) { return (unsigned)std::min<int64_t>(
-            ((int64_t)n + 256 * kUnroll - 1) / (256 * kUnroll), (int64_t)sms * 8); };
+        auto blocks = [&](const void *kernel, uint32_t n, int per_thread) {
+            return item_grid(kernel, n, per_thread, sms, per_thread == 1);
+        };
         if (flux_op == TSG_UPWIND)
-            iflux_pairs_kernel<TSG_UPWIND><<<blocks(nE), 256, 0, st>>>(e2v, nE, FastDiv(np), nlev, pd, vn, flux);
+            iflux_pairs_kernel<TSG_UPWIND><<<blocks((const void *)iflux_pairs_kernel<TSG_UPWIND>, nE, kUnroll), 256, 0,
+                                             st>>>(e2v, nE, FastDiv(np), nlev, pd, vn, flux);
         else
-            iflux_pairs_kernel<TSG_CENTRED><<<blocks(nE), 256, 0, st>>>(e2v, nE, FastDiv(np), nlev, pd, vn, flux);
-        ifluz_pairs_kernel<<<blocks(nZ), 256, 0, st>>>(nZ, FastDiv(np + 1), nlev, pivbz, pd, wn, fluz);
-        const unsigned bV = (unsigned)std::min<int64_t>(((int64_t)nV + 255) / 256, (int64_t)sms * 8);
+            iflux_pairs_kernel<TSG_CENTRED><<<blocks((const void *)iflux_pairs_kernel<TSG_CENTRED>, nE, kUnroll), 256,
+                                              0, st>>>(e2v, nE, FastDiv(np), nlev, pd, vn, flux);
+        ifluz_pairs_kernel<<<blocks((const void *)ifluz_pairs_kernel, nZ, kUnroll), 256, 0, st>>>(
+            nZ, FastDiv(np + 1), nlev, pivbz, pd, wn, fluz);
+        const unsigned bV = blocks((const void *)idiv_advance_pipe_kernel, nV, 1);
         idiv_advance_pipe_kernel<<<bV, 256, 0, st>>>(v2e, nV, FastDiv(np), nlev, dt, signs, dual, flux, fluz, pd,
                                                      rho, div, pd_out);
         TSG_CHECK_LAUNCH();
@@ -837,12 +859,12 @@ extern "C" int tsg_flat_flux(const int64_t *e2v, const double *pd, const double 
     if ((nlev & 1) == 0 && ne * (nlev / 2) < (1LL << 31) && a16(pd) && a16(vn) && a16(flux)) {
         const int np = nlev / 2;
         const uint32_t nE = (uint32_t)(ne * np);
-        const unsigned blocks = (unsigned)std::min<int64_t>(((int64_t)nE + 256 * kUnroll - 1) / (256 * kUnroll),
-                                                            (int64_t)sms * 8);
         if (flux_op == TSG_UPWIND)
-            iflux_pairs_kernel<TSG_UPWIND><<<blocks, 256, 0, st>>>(e2v, nE, FastDiv(np), nlev, pd, vn, flux);
+            iflux_pairs_kernel<TSG_UPWIND><<<item_grid((const void *)iflux_pairs_kernel<TSG_UPWIND>, nE, kUnroll,
+                                                           sms), 256, 0, st>>>(e2v, nE, FastDiv(np), nlev, pd, vn, flux);
         else
-            iflux_pairs_kernel<TSG_CENTRED><<<blocks, 256, 0, st>>>(e2v, nE, FastDiv(np), nlev, pd, vn, flux);
+            iflux_pairs_kernel<TSG_CENTRED><<<item_grid((const void *)iflux_pairs_kernel<TSG_CENTRED>, nE, kUnroll,
+                                                            sms), 256, 0, st>>>(e2v, nE, FastDiv(np), nlev, pd, vn, flux);
     } else if (flux_op == TSG_UPWIND) {
         launch_rows(iflux_kernel<TSG_UPWIND>, ne, sms, st, e2v, ne, nlev, pd, vn, flux);
     } else {

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <mutex>
 #include <unordered_map>
 
@@ -186,6 +187,23 @@ inline dim3 one_wave(const void *kernel, int64_t items, int num_sms) {
     return dim3((unsigned)(g < 1 ? 1 : g));
 }
 inline dim3 line_block() { return dim3(32, kWarps); }
+
+// grid of a grid-stride item kernel (256 threads, `per_thread` items per thread per pass).
+// Small sweeps: one wave of resident blocks (no tail wave).  Long sweeps (more than 16
+// passes of that wave): one pass per block instead.  Persistent blocks drift apart over
+// hundreds of passes, so a neighbour row fetched by one block is evicted from L2 before the
+// block that owns it arrives; blocks dispatched in index order keep one coherent wavefront.
+// The unfused step at O1280 (2560x2576x137): 25.7 vs 32.7 ms, its flux kernel reading
+// 36 vs 56 GB (ncu, tools/prof_unfused_o1280.py); at 279x256x80 (4 passes) the resident
+// wave stays ahead (162 vs 167 us).  `persistent` keeps the resident wave whatever the
+// length (kernels that prefetch their next item across passes).
+inline unsigned item_grid(const void *kernel, int64_t items, int per_thread, int num_sms,
+                          bool persistent = false) {
+    const int64_t need = (items + 256LL * per_thread - 1) / (256LL * per_thread);
+    const int64_t cap = (int64_t)num_sms * resident_blocks(kernel);
+    const int64_t g = (!persistent && need > 16 * cap) ? need : std::min(need, cap);
+    return (unsigned)std::max<int64_t>(1, g);
+}
 
 // launch an element-line kernel over `lines` (row, colour) lines of `cols` elements
 template <typename... Params, typename... Args>

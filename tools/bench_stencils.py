@@ -174,14 +174,13 @@ def launch_floor():
 
 if __name__ == "__main__":
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
-    launch_floor()
-    table1(128, 128, 80)
-    table1(1024, 1024, 80)
-    relations(256, 256, 80)
-    relations(1024, 1024, 80)
-    cell_div(256, 256, 80)
-    cell_div(1024, 1024, 80)
-    fusion(279, 256, 80)
-    fusion(2560, 2576, 137)
+    only = set(sys.argv[2].split(",")) if len(sys.argv) > 2 else None  # e.g. "fusion,table1"
+    for name, fn, args in (("floor", launch_floor, ()), ("table1", table1, (128, 128, 80)),
+                           ("table1", table1, (1024, 1024, 80)), ("relations", relations, (256, 256, 80)),
+                           ("relations", relations, (1024, 1024, 80)), ("cell_div", cell_div, (256, 256, 80)),
+                           ("cell_div", cell_div, (1024, 1024, 80)), ("fusion", fusion, (279, 256, 80)),
+                           ("fusion", fusion, (2560, 2576, 137))):
+        if only is None or name in only:
+            fn(*args)
     Path("gpurun_out").mkdir(exist_ok=True)
     Path(f"gpurun_out/stencils_{tag}.json").write_text(json.dumps(OUT, indent=1))
