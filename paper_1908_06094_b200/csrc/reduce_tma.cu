@@ -400,6 +400,16 @@ static int launch_compact(const tsg_grid *g, int inner, const double *src, const
             TSG_RV(1, 3, 8, 16, 16, 3)
             TSG_RV(2, 3, 4, 16, 16, 3)
         }
+    } else if constexpr (MODE != 0 && CT == 3) {  // cell divergence (edge source)
+        TSG_RV(1, 3, 4, 16, 16, 3)
+        TSG_RV(2, 3, 2, 16, 16, 4)
+        TSG_RV(3, 3, 4, 16, 16, 5)
+        TSG_RV(4, 3, 2, 16, 16, 3)
+        TSG_RV(5, 3, 4, 8, 16, 4)
+        TSG_RV(6, 3, 2, 32, 16, 3)
+        TSG_RV(7, 3, 8, 16, 16, 3)
+        TSG_RV(8, 3, 2, 16, 16, 6)
+        TSG_RV(9, 3, 4, 8, 16, 6)
     }
 #undef TSG_RV
     return launch_reduce_shape<REL, SCALE, MODE, RedCfg<CT, false>>(g, inner, src, scale, dst, st, length,
@@ -426,7 +436,10 @@ constexpr double kRedReuseUnits = 8.0;
 // while at 256x256x80 (~12 units per CTA) the static ranges are as fast or faster (EC 34.8
 // vs 37.1, EE 41.3 vs 44.5).  Dealt shapes per source location: 2 x 16 vertex tiles (8 CTAs
 // per SM), 4 x 16 cell and edge tiles, 8 x 16 edge tiles for V <- E (its 3 outputs per
-// thread want the wider tile: 1024^2 383 vs 450 us).
+// thread want the wider tile: 1024^2 383 vs 450 us).  The cell divergence (C <- E with
+// edge weights, a division per output in the simple form) takes 8 x 16 tiles too: 1024^2
+// simple / weighted 614 / 537 vs 673 / 587 us, 512x512x137 272 / 263 vs 286 / 261
+// (tools/reduce_variants.py celldiv, variant 17; bitwise equal).
 constexpr double kRedDynUnits = 24.0;
 
 template <int REL>
@@ -452,9 +465,13 @@ static int launch_reduce_tma(const tsg_grid *g, int inner, const double *src, co
     const double units = (double)((g->rows + C::TI - 1) / C::TI) * tiles_j * chunks;
     const double range = units / ((double)g->num_sms * per_sm), R = tiles_j * chunks;
     const double gap = R < range ? R : R - range * (double)(int64_t)(R / range);
-    if (!g_red_variant && range >= kRedDynUnits)
+    if (!g_red_variant && range >= kRedDynUnits) {
+        if constexpr (MODE != 0)
+            return launch_reduce_shape<REL, SCALE, MODE, RedShape<loc_colors(REL % 3), 8, 16>, false, true>(
+                g, inner, src, scale, dst, st, length, area, weights);
         return launch_reduce_shape<REL, SCALE, MODE, RedDynShape<REL>, false, true>(g, inner, src, scale, dst, st,
                                                                                    length, area, weights);
+    }
     if constexpr (REL == 0)
         if (!g_red_variant)
             return launch_reduce_shape<REL, SCALE, MODE, RedVVShape>(g, inner, src, scale, dst, st, length, area,

@@ -618,6 +618,39 @@ def test_tma_reduce_dynamic_deal_matches_oracle(cuda_ok):
     T.run_gpu(T.build_kernel(spec, fields, True))
     want = O.neighbor_sum_scaled(O.neighbor_table(r, c, "cells", "cells"), a, fac)
     assert np.array_equal(T.field_to_flat(fields["b"]), want)
+    _check_cell_divergence(spec, repeats=2)
+
+
+def _check_cell_divergence(spec, repeats=1, variants=(0,)):
+    """Both cell divergences (simple: a division per output; weighted) against the oracle,
+    bitwise, under each tsg_set_reduce_variant tile shape."""
+    from paper_1908_06094_b200 import _lib
+
+    r, c = spec.rows, spec.cols
+    geo, state = _case(spec, 3)
+    c2e = O.neighbor_table(r, c, "cells", "edges")
+    vn = T.field_to_flat(state.vn)
+    length = T.field_to_flat(geo.edge_length)[:, 0]
+    area = T.field_to_flat(geo.cell_area)[:, 0]
+    weights = geo.weights.core()[:, :, :, 0, :].reshape(-1, 3)
+    try:
+        for v in variants:
+            _lib.call("tsg_set_reduce_variant", v)
+            for weighted, want in ((False, O.cell_divergence(c2e, vn, length, area)),
+                                   (True, O.weighted_divergence(c2e, vn, weights))):
+                out = T.make_storage(spec, L.CELLS, "div_out")
+                for _ in range(repeats):
+                    T.run_gpu(T.build_divergence(spec, state, geo, weighted=weighted, out=out))
+                    assert np.array_equal(T.field_to_flat(out), want), (weighted, v)
+    finally:
+        _lib.call("tsg_set_reduce_variant", 0)
+
+
+def test_cell_divergence_every_tile_shape(cuda_ok):
+    """The cell divergence's benchmarking tile shapes (static 1-9, dealt 11-19) on a ragged
+    patch with an odd level count, and its default dealt 8 x 16 tile on a large patch."""
+    _check_cell_divergence(T.PatchSpec(37, 70, 35), variants=list(range(0, 10)) + list(range(11, 20)))
+    _check_cell_divergence(T.PatchSpec(300, 1030, 21))
 
 
 def test_tma_reduce_every_tile_shape(cuda_ok):

@@ -1,4 +1,4 @@
-"""ncu targets for the secondary kernels: python tools/prof_secondary.py {reduce_cc|reduce_vv|indirect|pack|unfused}."""
+"""ncu targets for the secondary kernels: python tools/prof_secondary.py {reduce_cc|reduce_vv|indirect|pack|unfused|celldiv_simple|celldiv_weighted}."""
 import sys
 sys.path.insert(0, "/root/repo")
 import torch
@@ -28,6 +28,15 @@ elif what == "pack":
     a = torch.rand((n, 80), dtype=torch.float64, device="cuda")
     f = g.empty(1, 80)
     fn = lambda: _lib.call("tsg_pack", g.handle, 1, 80, _lib.ptr(a), None, _lib.ptr(f), s)
+elif what.startswith("celldiv_"):
+    g = DeviceGrid(1024, 1024, 80)
+    vn, length, area, w, out = g.empty(2, 80), g.empty(2, 1), g.empty(1, 1), g.empty(1, 3), g.empty(1, 80)
+    for f, loc, inner, lo in ((vn, 2, 80, -0.5), (length, 2, 1, 0.5), (area, 1, 1, 0.5)):
+        _lib.call("tsg_fill_hash", g.handle, loc, inner, 4, lo, lo + 1.0, _lib.ptr(f), s)
+    _lib.call("tsg_cell_weights", g.handle, _lib.ptr(length), _lib.ptr(area), _lib.ptr(w), s)
+    weighted = int(what.endswith("weighted"))
+    fn = lambda: _lib.call("tsg_cell_divergence", g.handle, weighted, _lib.ptr(vn), _lib.ptr(length), _lib.ptr(area),
+                           _lib.ptr(w), _lib.ptr(out), s)
 elif what == "unfused":
     from paper_1908_06094_b200 import StructuredStepper
     from paper_1908_06094_b200.workloads import transport_inputs

@@ -4,6 +4,7 @@ the same bytes as the practical ceiling.  Every variant's output is checked bitw
 against the default shape's.  L2 flushed (256 MiB read) before every timed launch.
 
 usage: python tools/reduce_variants.py [rows cols K [variant,variant,...]]
+       python tools/reduce_variants.py celldiv rows cols K [variant,...]   (cell divergence)
 """
 
 from __future__ import annotations
@@ -43,7 +44,39 @@ def timed(fn, reps=200, warm=3):
     return sum(ts) / len(ts) / 1e3
 
 
+def cell_divergence(rows, cols, K, pick):
+    """The same A/B for tsg_cell_divergence (simple and weighted: cells <- edges with edge
+    weights; cell tile variants 1-9 static, 11-19 dealt)."""
+    g = DeviceGrid(rows, cols, K)
+    s = _lib.stream_handle()
+    vn, length, area, w = g.empty(2, K), g.empty(2, 1), g.empty(1, 1), g.empty(1, 3)
+    for f, loc, inner, lo in ((vn, 2, K, -0.5), (length, 2, 1, 0.5), (area, 1, 1, 0.5)):
+        _lib.call("tsg_fill_hash", g.handle, loc, inner, 4, lo, lo + 1.0, _lib.ptr(f), s)
+    _lib.call("tsg_cell_weights", g.handle, _lib.ptr(length), _lib.ptr(area), _lib.ptr(w), s)
+    nv = rows * cols
+    for weighted in (0, 1):
+        nbytes = (3 * nv + 2 * nv) * K * 8 + (2 * nv * 3 * 8 if weighted else (3 * nv + 2 * nv) * 8)
+        ref, out = g.empty(1, K), g.empty(1, K)
+        call = lambda o: _lib.call("tsg_cell_divergence", g.handle, weighted, _lib.ptr(vn), _lib.ptr(length),
+                                   _lib.ptr(area), _lib.ptr(w), _lib.ptr(o), s)
+        _lib.call("tsg_set_reduce_variant", 0)
+        call(ref)
+        for v in pick:
+            _lib.call("tsg_set_reduce_variant", v)
+            out.zero_()
+            tt = timed(lambda: call(out))
+            print(json.dumps(dict(name=f"cell_divergence_{'weighted' if weighted else 'simple'}", variant=v,
+                                  us=round(tt * 1e6, 2), frac=round(nbytes / tt / 1e9 / PEAK, 4),
+                                  bitwise=bool(torch.equal(out, ref)))), flush=True)
+        _lib.call("tsg_set_reduce_variant", 0)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "celldiv":  # celldiv rows cols K [variants]
+        rows, cols, K = (int(x) for x in sys.argv[2:5])
+        pick = [int(x) for x in sys.argv[5].split(",")] if len(sys.argv) > 5 else \
+            list(range(0, 10)) + list(range(11, 20))
+        return cell_divergence(rows, cols, K, pick)
     rows, cols, K = (int(x) for x in sys.argv[1:4]) if len(sys.argv) > 3 else (256, 256, 80)
     spec = PatchSpec(rows, cols, K)
     g = DeviceGrid(rows, cols, K)
