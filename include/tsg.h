@@ -243,8 +243,9 @@ int tsg_flat_cell_divergence(const int64_t *c2e, int width, const double *vn, co
  * warp. */
 int tsg_set_fused_variant(int variant);
 /* Benchmarking hook: force an alternative compact tile shape of the TMA neighbour reduce's
- * plain sum fold (1-9 static ranges, 11-19 the same shapes dynamically dealt); 0 (the
- * default) = the measured per-source-location shape and schedule. */
+ * plain sum fold and of the cell divergence (1-9 static ranges, 11-19 the same shapes
+ * dynamically dealt); 0 (the default) = the measured per-source-location shape and
+ * schedule. */
 int tsg_set_reduce_variant(int variant);
 int tsg_fused_variant_info(int variant, int *ti, int *tj, int *kc, int *stages, int *threads,
                            int *smem_bytes);
