@@ -102,7 +102,10 @@ __global__ void __launch_bounds__(TI *TJ * 8 + (MULTI ? 64 : 32), 1)
         prefetch_tmap(&tm_rho);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kWarps + (MULTI ? 1 : 0));  // MULTI: the signal warp too
+            // every consumer thread arrives (each read the stage's info slot; a per-warp
+            // arrival after __syncwarp orders the same, but compute-sanitizer's racecheck
+            // follows only the arriving thread's reads); MULTI: the signal warp's one too
+            mbar_init(&empty[s], kConsumers + (MULTI ? 1 : 0));
             mbar_init(&ibar[s], 1);
             if (MULTI) mbar_init(&dbar[s], kWarps);
         }
@@ -329,11 +332,11 @@ __global__ void __launch_bounds__(TI *TJ * 8 + (MULTI ? 64 : 32), 1)
                                                 reinterpret_cast<const double *>(sb + C::kRhoOff) + oR, vs, k,
                                                 a.K, a.dt, a.pivbz);
         }
-        __syncwarp();
-        if ((tid & 31) == 0) {
-            if (MULTI) mbar_arrive(&dbar[stage]);  // for the signal warp
-            mbar_arrive(&empty[stage]);
+        if constexpr (MULTI) {
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&dbar[stage]);  // for the signal warp
         }
+        mbar_arrive(&empty[stage]);
     }
     if (a.trace && tid == 0) {
         a.trace[4 * blockIdx.x + 2] = globaltimer_ns();
