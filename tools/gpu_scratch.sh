@@ -1,14 +1,5 @@
-for sz in 19x40x36 200x400x36; do
-timeout 1800 compute-sanitizer --tool racecheck --racecheck-report all --print-limit 20 python tools/sanitize_dyn.py $sz > gpurun_out/san_dyn_racecheck_$sz.log 2>&1; echo "$sz rc=$?"; tail -2 gpurun_out/san_dyn_racecheck_$sz.log
+for tool in memcheck synccheck; do
+timeout 1800 compute-sanitizer --tool $tool python tools/sanitize_dyn.py 200x400x36 > gpurun_out/san_dyn_$tool.log 2>&1; echo "$tool rc=$?"; tail -1 gpurun_out/san_dyn_$tool.log
 done
-timeout 1800 compute-sanitizer --tool racecheck python tools/sanitize_stencils.py 2>&1 | tail -2
-for rep in 1 2; do for lib in libtsg_prev.so libtsg.so; do
-TSG_LIBRARY=$PWD/paper_1908_06094_b200/$lib timeout 600 python bench.py --no-cpu --cpu-seconds 0 --sustained-seconds 0 > gpurun_out/bh_$lib.json 2>gpurun_out/bh_$lib.err
-python - "$lib" <<'PY'
-import json,sys
-d=json.loads([l for l in open(f"gpurun_out/bh_{sys.argv[1]}.json") if l.startswith('{')][-1])
-o=d['o1280_strong']
-print(sys.argv[1], 'loop %.2f us %.3f'%(d['ms_per_step']*1e3, d['roofline']['frac']), 'flushed %.2f'%(d['step_flushed']['ms_per_step']*1e3),
-      'o1280 %.2f ms (%.3f) iso %.2f'%(o['ms_per_step'], o['roofline_frac'], o['isolated_step']['ms_per_step']))
-PY
-done; done
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
