@@ -556,6 +556,9 @@ __global__ void __launch_bounds__(256) iflux_pairs_kernel(const int64_t *__restr
 // 155.3 -> 149.0 us, 1024x1024x80 2112 -> 1993 us (tools/indirect_step_variants.py,
 // TSG_IPIPE A/B build, bitwise unchanged); the same for the two-row edge flux gather
 // lost (157.4 / 2126 us), so that stage keeps four items per thread.
+// ADV = false: the divergence alone (the reference's flux_divergence, reference.py:63-79,
+// for callers of the per-stage functions); pd / rho / pd_out are then unused.
+template <bool ADV>
 __global__ void __launch_bounds__(256) idiv_advance_pipe_kernel(
     const int64_t *__restrict__ v2e, uint32_t n, FastDiv np, int K, double dt,
     const double *__restrict__ signs, const double *__restrict__ dual, const double *__restrict__ flux,
@@ -593,8 +596,86 @@ __global__ void __launch_bounds__(256) idiv_advance_pipe_kernel(
         const double2 d = make_double2(dvd(acc.x, du), dvd(acc.y, du));
         const int64_t qq = (int64_t)vc * K + k;
         st2(div + qq, d);
-        const double2 r = ld2(rho + qq), p = ld2(pd + qq);
-        st2(pd_out + qq, make_double2(sub(p.x, dvd(mul(dt, d.x), r.x)), sub(p.y, dvd(mul(dt, d.y), r.y))));
+        if constexpr (ADV) {
+            const double2 r = ld2(rho + qq), p = ld2(pd + qq);
+            st2(pd_out + qq, make_double2(sub(p.x, dvd(mul(dt, d.x), r.x)), sub(p.y, dvd(mul(dt, d.y), r.y))));
+        }
+    }
+}
+
+// The table-driven cell divergence (reference.cell_divergence, reference.py:119-134) in
+// level-pair items, pipelined like the Table-1 gather: the table row of the item after
+// next and the edge lengths of the next item (they depend on its table row, fetched one
+// iteration earlier) are in flight while the current item's vn pairs are.
+#ifndef TSG_CDIV_DEPTH  // A/B builds only
+#define TSG_CDIV_DEPTH 2
+#endif
+__global__ void __launch_bounds__(256) icell_div_pipe_kernel(const int64_t *__restrict__ c2e, uint32_t n,
+                                                             FastDiv np, int K, const double *__restrict__ vn,
+                                                             const double *__restrict__ length,
+                                                             const double *__restrict__ area,
+                                                             double *__restrict__ out) {
+    const uint32_t T = gridDim.x * blockDim.x;
+    uint32_t it = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t c = 0, c1 = 0;
+    int64_t nb[3], nb1[3];
+    double ln[3], ar = 1.0;
+    auto rows = [&](uint32_t i, uint32_t &cc, int64_t *q) {
+        cc = np.div(i);
+#pragma unroll
+        for (int s = 0; s < 3; ++s) q[s] = __ldg(c2e + (int64_t)cc * 3 + s);
+    };
+    auto weights = [&](uint32_t cc, const int64_t *q) {
+#pragma unroll
+        for (int s = 0; s < 3; ++s) ln[s] = __ldg(length + q[s]);
+        ar = __ldg(area + cc);
+    };
+    if (it < n) {
+        rows(it, c, nb);
+        weights(c, nb);
+        if (TSG_CDIV_DEPTH == 2 && it + T < n) rows(it + T, c1, nb1);
+    }
+    for (; it < n; it += T) {
+        const int k = 2 * (it - c * np.d);
+        const uint32_t cc = c;
+        double2 v[3];
+        double l[3];
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+            v[s] = ld2(vn + nb[s] * K + k);
+            l[s] = ln[s];
+        }
+        const double a = ar;
+        if (it + T < n) {
+            if (TSG_CDIV_DEPTH == 2) {
+                c = c1;
+#pragma unroll
+                for (int s = 0; s < 3; ++s) nb[s] = nb1[s];
+                weights(c, nb);
+                if (it + 2 * T < n) rows(it + 2 * T, c1, nb1);
+            } else {
+                rows(it + T, c, nb);
+                weights(c, nb);
+            }
+        }
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+            acc.x = add(mul(v[s].x, l[s]), acc.x);
+            acc.y = add(mul(v[s].y, l[s]), acc.y);
+        }
+        st2(out + (int64_t)cc * K + k, make_double2(dvd(acc.x, a), dvd(acc.y, a)));
+    }
+}
+
+// The explicit update over value pairs (16-byte loads and stores)
+__global__ void __launch_bounds__(256) advance_flat2_kernel(int64_t n2, double dt, const double *__restrict__ pd,
+                                                            const double *__restrict__ div,
+                                                            const double *__restrict__ rho,
+                                                            double *__restrict__ out) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n2; q += (int64_t)gridDim.x * blockDim.x) {
+        const double2 d = ld2(div + 2 * q), r = ld2(rho + 2 * q), p = ld2(pd + 2 * q);
+        st2(out + 2 * q, make_double2(sub(p.x, dvd(mul(dt, d.x), r.x)), sub(p.y, dvd(mul(dt, d.y), r.y))));
     }
 }
 
@@ -828,8 +909,8 @@ extern "C" int tsg_transport_indirect(const int64_t *e2v, const int64_t *v2e, co
                                               0, st>>>(e2v, nE, FastDiv(np), nlev, pd, vn, flux);
         ifluz_pairs_kernel<<<blocks((const void *)ifluz_pairs_kernel, nZ, kUnroll), 256, 0, st>>>(
             nZ, FastDiv(np + 1), nlev, pivbz, pd, wn, fluz);
-        const unsigned bV = blocks((const void *)idiv_advance_pipe_kernel, nV, 1);
-        idiv_advance_pipe_kernel<<<bV, 256, 0, st>>>(v2e, nV, FastDiv(np), nlev, dt, signs, dual, flux, fluz, pd,
+        const unsigned bV = blocks((const void *)idiv_advance_pipe_kernel<true>, nV, 1);
+        idiv_advance_pipe_kernel<true><<<bV, 256, 0, st>>>(v2e, nV, FastDiv(np), nlev, dt, signs, dual, flux, fluz, pd,
                                                      rho, div, pd_out);
         TSG_CHECK_LAUNCH();
         return TSG_OK;
@@ -880,7 +961,14 @@ extern "C" int tsg_flat_fluz(const double *pd, const double *wn, int64_t nv, int
     if (nlev < 2) return fail(TSG_EVALUE, "need at least 2 levels, got %d", nlev);
     if (nv < 0) return fail(TSG_EVALUE, "bad vertex count %lld", (long long)nv);
     if (nv == 0) return TSG_OK;
-    launch_rows(ifluz_kernel, nv, sm_count(), (cudaStream_t)s, nv, nlev, pivbz, pd, wn, fluz);
+    const int np = nlev / 2 + 1;  // interface pairs covering 0..nlev
+    if (nv * np < (1LL << 31)) {
+        const uint32_t n = (uint32_t)(nv * np);
+        ifluz_pairs_kernel<<<item_grid((const void *)ifluz_pairs_kernel, n, kUnroll, sm_count()), 256, 0,
+                             (cudaStream_t)s>>>(n, FastDiv(np), nlev, pivbz, pd, wn, fluz);
+    } else {
+        launch_rows(ifluz_kernel, nv, sm_count(), (cudaStream_t)s, nv, nlev, pivbz, pd, wn, fluz);
+    }
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }
@@ -892,7 +980,16 @@ extern "C" int tsg_flat_divergence(const int64_t *v2e, int width, const double *
     if (nv < 0 || width < 0 || nlev < 1)
         return fail(TSG_EVALUE, "bad shape (nv=%lld, width %d, levels %d)", (long long)nv, width, nlev);
     if (nv == 0) return TSG_OK;
-    launch_rows(idiv_kernel, nv, sm_count(), (cudaStream_t)s, v2e, width, nv, nlev, signs, dual, flux, fluz, div);
+    auto a16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) % 16) == 0; };
+    if (width == 6 && (nlev & 1) == 0 && nv * (nlev / 2) < (1LL << 31) && a16(flux) && a16(div)) {
+        const uint32_t n = (uint32_t)(nv * (nlev / 2));
+        idiv_advance_pipe_kernel<false><<<item_grid((const void *)idiv_advance_pipe_kernel<false>, n, 1, sm_count(),
+                                                    true), 256, 0, (cudaStream_t)s>>>(
+            v2e, n, FastDiv(nlev / 2), nlev, 0.0, signs, dual, flux, fluz, nullptr, nullptr, div, nullptr);
+    } else {
+        launch_rows(idiv_kernel, nv, sm_count(), (cudaStream_t)s, v2e, width, nv, nlev, signs, dual, flux, fluz,
+                    div);
+    }
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }
@@ -902,8 +999,14 @@ extern "C" int tsg_flat_advance(const double *pd, const double *div, const doubl
     if (!pd || !div || !rho || !pd_out) return fail(TSG_EVALUE, "tsg_flat_advance: NULL array");
     if (n < 0) return fail(TSG_EVALUE, "bad value count %lld", (long long)n);
     if (n == 0) return TSG_OK;
-    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
-    advance_flat_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)s>>>(n, dt, pd, div, rho, pd_out);
+    auto a16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) % 16) == 0; };
+    if ((n & 1) == 0 && a16(pd) && a16(div) && a16(rho) && a16(pd_out)) {
+        advance_flat2_kernel<<<item_grid((const void *)advance_flat2_kernel, n / 2, 1, sm_count()), 256, 0,
+                               (cudaStream_t)s>>>(n / 2, dt, pd, div, rho, pd_out);
+    } else {
+        const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
+        advance_flat_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)s>>>(n, dt, pd, div, rho, pd_out);
+    }
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }
@@ -914,7 +1017,15 @@ extern "C" int tsg_flat_cell_divergence(const int64_t *c2e, int width, const dou
     if (nc < 0 || width < 0 || nlev < 1)
         return fail(TSG_EVALUE, "bad shape (nc=%lld, width %d, levels %d)", (long long)nc, width, nlev);
     if (nc == 0) return TSG_OK;
-    launch_rows(icell_div_kernel, nc, sm_count(), (cudaStream_t)s, c2e, width, nc, nlev, vn, length, area, out);
+    auto a16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) % 16) == 0; };
+    if (width == 3 && (nlev & 1) == 0 && nc * (nlev / 2) < (1LL << 31) && a16(vn) && a16(out)) {
+        const uint32_t n = (uint32_t)(nc * (nlev / 2));
+        icell_div_pipe_kernel<<<item_grid((const void *)icell_div_pipe_kernel, n, 1, sm_count(), true), 256, 0,
+                                (cudaStream_t)s>>>(c2e, n, FastDiv(nlev / 2), nlev, vn, length, area, out);
+    } else {
+        launch_rows(icell_div_kernel, nc, sm_count(), (cudaStream_t)s, c2e, width, nc, nlev, vn, length, area,
+                    out);
+    }
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }

@@ -65,6 +65,36 @@ def test_flat_stages_match_oracle(cuda_ok, shape, relabel):
     assert np.array_equal(R.neighbor_sum_scaled(c2c, a, fac), O.neighbor_sum_scaled(c2c, a, fac))
 
 
+def test_flat_stages_long_sweeps(cuda_ok):
+    """A patch whose level-pair sweeps are long enough for one-pass grids (tsg_common.cuh
+    item_grid) and the pipelined divergence / cell-divergence gathers: each stage, bitwise."""
+    import torch
+
+    r, c, k = 1024, 1024, 40
+    inp = O.transport_inputs(r, c, k, 2, "random", "random", "random")
+    e2v = O.neighbor_table(r, c, "edges", "vertices")
+    v2e = O.neighbor_table(r, c, "vertices", "edges")
+    c2e = O.neighbor_table(r, c, "cells", "edges")
+    dev = {n: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+           for n, x in (("e2v", e2v), ("v2e", v2e), ("c2e", c2e), ("pd", inp["pd"]), ("vn", inp["vn"]),
+                        ("wn", inp["wn"]), ("rho", inp["rho"]), ("signs", inp["signs"]),
+                        ("dual", inp["dual"].reshape(-1)))}
+    flux = O.upwind_flux(e2v, inp["vn"], inp["pd"])
+    fluz = O.upwind_fluz(inp["wn"], inp["pd"], 0.5)
+    got = R.upwind_fluz(dev["wn"], dev["pd"], 0.5)
+    assert np.array_equal(got.cpu().numpy(), fluz)
+    div = O.flux_divergence(v2e, inp["signs"], inp["dual"].reshape(-1), flux, fluz)
+    got = R.flux_divergence(dev["v2e"], dev["signs"], dev["dual"], torch.from_numpy(flux).cuda(),
+                            torch.from_numpy(fluz).cuda())
+    assert np.array_equal(got.cpu().numpy(), div)
+    out = R.advance_density(dev["pd"], torch.from_numpy(div).cuda(), dev["rho"], 0.1)
+    assert np.array_equal(out.cpu().numpy(), O.advance_density(inp["pd"], div, inp["rho"], 0.1))
+    length = 0.5 + np.random.default_rng(3).random(len(e2v))
+    area = 0.2 + np.random.default_rng(4).random(len(c2e))
+    got = R.cell_divergence(dev["c2e"], dev["vn"], torch.from_numpy(length).cuda(), torch.from_numpy(area).cuda())
+    assert np.array_equal(got.cpu().numpy(), O.cell_divergence(c2e, inp["vn"], length, area))
+
+
 def test_one_dimensional_arrays_and_device_tensors(cuda_ok):
     import torch
 

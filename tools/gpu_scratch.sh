@@ -1,5 +1,5 @@
-for tool in memcheck synccheck; do
-timeout 1800 compute-sanitizer --tool $tool python tools/sanitize_dyn.py 200x400x36 > gpurun_out/san_dyn_$tool.log 2>&1; echo "$tool rc=$?"; tail -1 gpurun_out/san_dyn_$tool.log
-done
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+for rep in 1 2; do for lib in libtsg.so libtsg_d1.so; do echo "== $lib"
+TSG_LIBRARY=$PWD/paper_1908_06094_b200/$lib timeout 600 python tools/flat_stages_probe.py 2>&1 | grep cell_div
+TSG_LIBRARY=$PWD/paper_1908_06094_b200/$lib timeout 600 python tools/flat_stages_probe.py 279 256 80 2>&1 | grep cell_div
+done; done
+timeout 900 python -m pytest tests/test_gpu_reference_api.py -x -q 2>&1 | tail -2
