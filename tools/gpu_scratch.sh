@@ -1,8 +1,10 @@
-bash tools/gpu_round.sh > gpurun_out/round.log 2>&1
-cp gpurun_out/bench.log gpurun_out/bench_r2e.log; cp gpurun_out/bench_ref.log gpurun_out/bench_ref_r2e.log
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-    --log-file gpurun_out/launches_r2e.csv python bench.py --steps 20 --warmup 5 --no-cpu --no-o1280 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:mpdata_dyn -s 1 -c 1 \
-    -o gpurun_out/prof_r2e -f python tools/prof_loop.py 10 > gpurun_out/ncu_r2e.log 2>&1
-timeout 900 python tools/bench_stencils.py r2f > gpurun_out/stencils_r2f.log 2>&1
-tail -30 gpurun_out/round.log
+for rep in 1 2; do for lib in libtsg.so libtsg_a4.so; do
+TSG_LIBRARY=$PWD/paper_1908_06094_b200/$lib timeout 600 python bench.py --no-cpu --cpu-seconds 0 --sustained-seconds 0 > gpurun_out/bh_$lib.json 2>gpurun_out/bh_$lib.err
+python - "$lib" <<'PY'
+import json,sys
+d=json.loads([l for l in open(f"gpurun_out/bh_{sys.argv[1]}.json") if l.startswith('{')][-1])
+o=d['o1280_strong']
+print(sys.argv[1], 'loop %.2f us %.3f'%(d['ms_per_step']*1e3, d['roofline']['frac']), 'flushed %.2f'%(d['step_flushed']['ms_per_step']*1e3),
+      'o1280 %.2f ms (%.3f) iso %.2f'%(o['ms_per_step'], o['roofline_frac'], o['isolated_step']['ms_per_step']))
+PY
+done; done
