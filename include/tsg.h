@@ -247,6 +247,11 @@ int tsg_set_fused_variant(int variant);
  * dynamically dealt); 0 (the default) = the measured per-source-location shape and
  * schedule. */
 int tsg_set_reduce_variant(int variant);
+/* Testing hook: the number of points (elements x levels) one launch of the point-indexed
+ * kernels (reorders, synthetic fill, the unfused step's level-pair items) covers before
+ * the field is split into row bands; 0 restores the default 2^32 - 2^24.  Process-wide.
+ * No reference counterpart. */
+int tsg_set_point_limit(int64_t n);
 int tsg_fused_variant_info(int variant, int *ti, int *tj, int *kc, int *stages, int *threads,
                            int *smem_bytes);
 /* The variant a fused launch over logical rows [row_lo, row_hi) of `g` uses (-1 on error). */

@@ -61,6 +61,7 @@ SIGNATURES = {
     "tsg_mpdata_run": (_c_int, [_p] + [_p] * 7 + [_c_dbl, _c_dbl, _c_int, _c_int, _p]),
     "tsg_set_fused_variant": (_c_int, [_c_int]),
     "tsg_set_reduce_variant": (_c_int, [_c_int]),
+    "tsg_set_point_limit": (_c_int, [_c_i64]),
     "tsg_fused_variant_of": (_c_int, [_p, _c_int, _c_int]),
     "tsg_fused_band_of": (_c_int, [_p, _c_int, _c_int]),
     "tsg_set_fused_band": (_c_int, [_c_int]),

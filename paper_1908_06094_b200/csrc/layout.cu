@@ -489,18 +489,21 @@ extern "C" int tsg_pack(const tsg_grid *g, int loc, int inner, const double *fla
     if (!valid_loc(loc) || inner < 1) return fail(TSG_EVALUE, "tsg_pack: bad location/inner");
     if (!flat || !field) return fail(TSG_EVALUE, "tsg_pack: NULL array");
     FieldIx F(g->rows, g->cols, colors_of(loc), inner);
-    if (!PointDec::fits(g->rows, g->cols, F.colors, inner)) return fail(TSG_EVALUE, "field too large");
-    PointDec D(g->rows, g->cols, F.colors, inner);
     if (pairs_ok(inner, flat)) {
-        PointDec Dp(g->rows, g->cols, F.colors, inner / 2);
-        pack_pairs_kernel<kPackUnroll><<<grid_for((Dp.n + kPackUnroll - 1) / kPackUnroll, 256, g->num_sms),
-                                         256, 0, (cudaStream_t)s>>>(F, inner, Dp, flat, forward, field, g->flags);
-    } else if (inner >= 16)
+        for_point_bands(g->rows, g->cols, F.colors, inner / 2, [&](const PointDec &Dp) {
+            pack_pairs_kernel<kPackUnroll><<<grid_for((Dp.n + kPackUnroll - 1) / kPackUnroll, 256, g->num_sms),
+                                             256, 0, (cudaStream_t)s>>>(F, inner, Dp, flat, forward, field,
+                                                                        g->flags);
+        });
+    } else if (inner >= 16) {
         launch_lines(pack_lines_kernel, g->cols, (int64_t)g->rows * F.colors, g->num_sms,
                      (cudaStream_t)s, F, inner, flat, forward, field, g->flags);
-    else
-        pack_kernel<<<grid_for(D.n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(F, inner, D, flat,
-                                                                                 forward, field, g->flags);
+    } else {
+        for_point_bands(g->rows, g->cols, F.colors, inner, [&](const PointDec &D) {
+            pack_kernel<<<grid_for(D.n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(F, inner, D, flat,
+                                                                                     forward, field, g->flags);
+        });
+    }
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }
@@ -511,18 +514,20 @@ extern "C" int tsg_unpack(const tsg_grid *g, int loc, int inner, const double *f
     if (!valid_loc(loc) || inner < 1) return fail(TSG_EVALUE, "tsg_unpack: bad location/inner");
     if (!flat || !field) return fail(TSG_EVALUE, "tsg_unpack: NULL array");
     FieldIx F(g->rows, g->cols, colors_of(loc), inner);
-    if (!PointDec::fits(g->rows, g->cols, F.colors, inner)) return fail(TSG_EVALUE, "field too large");
-    PointDec D(g->rows, g->cols, F.colors, inner);
     if (pairs_ok(inner, flat)) {
-        PointDec Dp(g->rows, g->cols, F.colors, inner / 2);
-        unpack_pairs_kernel<<<grid_for((Dp.n + kItemUnroll - 1) / kItemUnroll, 256, g->num_sms), 256, 0,
-                              (cudaStream_t)s>>>(F, inner, Dp, field, forward, flat);
-    } else if (inner >= 16)
+        for_point_bands(g->rows, g->cols, F.colors, inner / 2, [&](const PointDec &Dp) {
+            unpack_pairs_kernel<<<grid_for((Dp.n + kItemUnroll - 1) / kItemUnroll, 256, g->num_sms), 256, 0,
+                                  (cudaStream_t)s>>>(F, inner, Dp, field, forward, flat);
+        });
+    } else if (inner >= 16) {
         launch_lines(unpack_lines_kernel, g->cols, (int64_t)g->rows * F.colors, g->num_sms,
                      (cudaStream_t)s, F, inner, field, forward, flat);
-    else
-        unpack_kernel<<<grid_for(D.n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(F, inner, D, field,
-                                                                                   forward, flat);
+    } else {
+        for_point_bands(g->rows, g->cols, F.colors, inner, [&](const PointDec &D) {
+            unpack_kernel<<<grid_for(D.n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(F, inner, D, field,
+                                                                                       forward, flat);
+        });
+    }
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }
@@ -546,10 +551,10 @@ extern "C" int tsg_fill_hash(const tsg_grid *g, int loc, int inner, uint64_t see
     if (!valid_loc(loc) || inner < 1) return fail(TSG_EVALUE, "tsg_fill_hash: bad location/inner");
     if (!field) return fail(TSG_EVALUE, "tsg_fill_hash: NULL field");
     FieldIx F(g->rows, g->cols, colors_of(loc), inner);
-    if (!PointDec::fits(g->rows, g->cols, F.colors, inner)) return fail(TSG_EVALUE, "field too large");
-    PointDec D(g->rows, g->cols, F.colors, inner);
-    fill_hash_kernel<<<grid_for(D.n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(
-        F, inner, D, g->row0, seed, lo, hi, field, g->flags);
+    for_point_bands(g->rows, g->cols, F.colors, inner, [&](const PointDec &D) {
+        fill_hash_kernel<<<grid_for(D.n, 256, g->num_sms), 256, 0, (cudaStream_t)s>>>(
+            F, inner, D, g->row0, seed, lo, hi, field, g->flags);
+    });
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }

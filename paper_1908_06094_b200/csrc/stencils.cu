@@ -207,92 +207,10 @@ __global__ void __launch_bounds__(256) cell_div_kernel(FieldIx Fvn, FieldIx Fl, 
 
 // -- unfused MPDATA (run_naive analogue, executors.py:213-245) --------------------------
 
-template <int OP>
-__global__ void __launch_bounds__(256) flux_kernel(FieldIx Fp, FieldIx Fe, int K,
-                                                   const double *__restrict__ pd,
-                                                   const double *__restrict__ vn,
-                                                   double *__restrict__ flux, int flags) {
-    TSG_LINES(Fe, i, c, j) {
-        // E->V slot 1 (connectivity.py:38-42): c0 (0,+1), c1 (+1,+1), c2 (+1,0)
-        const double *po = pd + Fp.at(i, 0, j);
-        const double *pp = pd + Fp.at(i + (c == 0 ? 0 : 1), 0, j + (c == 2 ? 0 : 1));
-        const double *v = vn + Fe.at(i, c, j);
-        double *o = flux + Fe.at(i, c, j);
-        const Img m = images(Fe, i, j, flags);
-        for (int k = threadIdx.x; k < K; k += 32) put(o, m, k, edge_flux<OP>(po[k], pp[k], v[k]));
-    }
-}
-
-__global__ void __launch_bounds__(256) fluz_kernel(FieldIx Fp, FieldIx Fw, int K, double pivbz,
-                                                   const double *__restrict__ pd,
-                                                   const double *__restrict__ wn,
-                                                   double *__restrict__ fluz, int flags) {
-    TSG_LINES(Fp, i, c, j) {
-        const double *P = pd + Fp.at(i, 0, j);
-        const double *W = wn + Fw.at(i, 0, j);
-        double *o = fluz + Fw.at(i, 0, j);
-        const Img m = images(Fw, i, j, flags);
-        for (int k = threadIdx.x; k <= K; k += 32) {
-            double f;
-            if (k == 0) f = mul(pivbz, fluz_interior(W[1], P[0], P[1]));
-            else if (k == K) f = mul(pivbz, fluz_interior(W[K - 1], P[K - 2], P[K - 1]));
-            else f = fluz_interior(W[k], P[k - 1], P[k]);
-            put(o, m, k, f);
-        }
-    }
-}
-
-__global__ void __launch_bounds__(256) div_kernel(FieldIx Fe, FieldIx Fw, FieldIx Fs, FieldIx Fd,
-                                                  FieldIx Fv, int K, const double *__restrict__ flux,
-                                                  const double *__restrict__ fluz,
-                                                  const double *__restrict__ signs,
-                                                  const double *__restrict__ dual,
-                                                  double *__restrict__ divvd, int flags) {
-    constexpr int REL = TSG_VERTICES * 3 + TSG_EDGES;
-    TSG_LINES(Fv, i, c, j) {
-        const double *f[6];
-        double sg[6];
-        const double *S = signs + Fs.at(i, 0, j);
-#pragma unroll
-        for (int s = 0; s < 6; ++s) {
-            const int8_t *o = c_offsets[REL][0][s];
-            f[s] = flux + Fe.at(i + o[0], o[1], j + o[2]);
-            sg[s] = S[s];
-        }
-        const double *Z = fluz + Fw.at(i, 0, j);
-        const double du = dual[Fd.at(i, 0, j)];
-        double *o = divvd + Fv.at(i, 0, j);
-        const Img m = images(Fv, i, j, flags);
-        for (int k = threadIdx.x; k < K; k += 32) {
-            double acc = 0.0;
-#pragma unroll
-            for (int s = 0; s < 6; ++s) acc = add(mul(sg[s], f[s][k]), acc);
-            acc = add(acc, sub(Z[k + 1], Z[k]));
-            put(o, m, k, dvd(acc, du));
-        }
-    }
-}
-
-__global__ void __launch_bounds__(256) advance_kernel(FieldIx Fv, int K, double dt,
-                                                      const double *__restrict__ pd,
-                                                      const double *__restrict__ divvd,
-                                                      const double *__restrict__ rho,
-                                                      double *__restrict__ pd_out, int flags) {
-    TSG_LINES(Fv, i, c, j) {
-        const int64_t e = Fv.at(i, 0, j);
-        const Img m = images(Fv, i, j, flags);
-        for (int k = threadIdx.x; k < K; k += 32) {
-            double slope = mul(dt, divvd[e + k]);
-            slope = dvd(slope, rho[e + k]);
-            put(pd_out + e, m, k, sub(pd[e + k], slope));
-        }
-    }
-}
-
 // Level-pair item forms of the four unfused stages: one thread per
 // (element, level pair) over the whole field, kUnroll items per thread per pass, 16-byte
-// loads and stores -- the element-line forms above are latency-bound with a quarter of
-// their lanes idle in the last pass of an 80-level run.  Item order: on a resident grid
+// loads and stores (round 1's element-line forms, one warp per element, were latency-bound
+// with a quarter of their lanes idle in the last pass of an 80-level run).  Item order: on a resident grid
 // (item_grid, short sweeps) thread t's items of a pass are t, t + T, ... (T = all threads);
 // on a one-pass grid (long sweeps) the stencil stages take a block's kUnroll x 256 items
 // contiguously instead, so the items in flight form one wavefront rather than kUnroll
@@ -846,37 +764,32 @@ extern "C" int tsg_mpdata_step_unfused(const tsg_grid *g, const double *pd, cons
     FieldIx Fv(g->rows, g->cols, 1, K), Fe(g->rows, g->cols, 3, K), Fw(g->rows, g->cols, 1, K + 1),
         Fs(g->rows, g->cols, 1, 6), Fd(g->rows, g->cols, 1, 1);
     const int C = g->cols, sms = g->num_sms;
-    const int64_t lE = 3LL * g->rows, lV = g->rows;
-    if (PointDec::fits(g->rows, C, 3, K + 1)) {  // level-pair items
-        // an odd level count's last pair ends in the padding of every field (even pitch)
-        const int np = (K + 1) / 2;
-        const PointDec DV(g->rows, C, 1, np), DZ(g->rows, C, 1, K / 2 + 1);
-        auto blocks = [&](const void *kernel, const PointDec &D) {
-            return item_grid(kernel, D.n, kUnroll, sms);
-        };
-        if (flux_op == TSG_UPWIND)
-            flux3_pairs_kernel<TSG_UPWIND><<<blocks((const void *)flux3_pairs_kernel<TSG_UPWIND>, DV), 256, 0, st>>>(
-                Fv, Fe, DV, pd, vn, flux, g->flags);
-        else
-            flux3_pairs_kernel<TSG_CENTRED><<<blocks((const void *)flux3_pairs_kernel<TSG_CENTRED>, DV), 256, 0, st>>>(
-                Fv, Fe, DV, pd, vn, flux, g->flags);
-        fluz_pairs_kernel<<<blocks((const void *)fluz_pairs_kernel, DZ), 256, 0, st>>>(Fv, Fw, DZ, K, pivbz, pd, wn,
-                                                                                       fluz, g->flags);
-        div_pairs_kernel<<<blocks((const void *)div_pairs_kernel, DV), 256, 0, st>>>(
-            Fe, Fw, Fs, Fd, Fv, DV, flux, fluz, signs, dual, divvd, g->flags);
-        advance_pairs_kernel<<<blocks((const void *)advance_pairs_kernel, DV), 256, 0, st>>>(Fv, DV, dt, pd, divvd,
-                                                                                             rho, pd_out, g->flags);
-        TSG_CHECK_LAUNCH();
-        return TSG_OK;
-    }
+    // level-pair items; an odd level count's last pair ends in the padding of every field
+    // (even pitch).  Each stage runs over row bands of at most point_limit() items (one
+    // band up to ~62 M vertices at 137 levels) before the next stage starts.
+    const int np = (K + 1) / 2;
+    auto stage = [&](auto kernel, int pairs, auto launch) {
+        for_point_bands(g->rows, C, 1, pairs, [&](const PointDec &D) {
+            launch(item_grid((const void *)kernel, D.n, kUnroll, sms), D);
+        });
+    };
     if (flux_op == TSG_UPWIND)
-        launch_lines(flux_kernel<TSG_UPWIND>, C, lE, sms, st, Fv, Fe, K, pd, vn, flux, g->flags);
+        stage(flux3_pairs_kernel<TSG_UPWIND>, np, [&](unsigned b, const PointDec &D) {
+            flux3_pairs_kernel<TSG_UPWIND><<<b, 256, 0, st>>>(Fv, Fe, D, pd, vn, flux, g->flags);
+        });
     else
-        launch_lines(flux_kernel<TSG_CENTRED>, C, lE, sms, st, Fv, Fe, K, pd, vn, flux, g->flags);
-    launch_lines(fluz_kernel, C, lV, sms, st, Fv, Fw, K, pivbz, pd, wn, fluz, g->flags);
-    launch_lines(div_kernel, C, lV, sms, st, Fe, Fw, Fs, Fd, Fv, K, flux, fluz, signs, dual, divvd,
-                 g->flags);
-    launch_lines(advance_kernel, C, lV, sms, st, Fv, K, dt, pd, divvd, rho, pd_out, g->flags);
+        stage(flux3_pairs_kernel<TSG_CENTRED>, np, [&](unsigned b, const PointDec &D) {
+            flux3_pairs_kernel<TSG_CENTRED><<<b, 256, 0, st>>>(Fv, Fe, D, pd, vn, flux, g->flags);
+        });
+    stage(fluz_pairs_kernel, K / 2 + 1, [&](unsigned b, const PointDec &D) {
+        fluz_pairs_kernel<<<b, 256, 0, st>>>(Fv, Fw, D, K, pivbz, pd, wn, fluz, g->flags);
+    });
+    stage(div_pairs_kernel, np, [&](unsigned b, const PointDec &D) {
+        div_pairs_kernel<<<b, 256, 0, st>>>(Fe, Fw, Fs, Fd, Fv, D, flux, fluz, signs, dual, divvd, g->flags);
+    });
+    stage(advance_pairs_kernel, np, [&](unsigned b, const PointDec &D) {
+        advance_pairs_kernel<<<b, 256, 0, st>>>(Fv, D, dt, pd, divvd, rho, pd_out, g->flags);
+    });
     TSG_CHECK_LAUNCH();
     return TSG_OK;
 }

@@ -3,6 +3,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
 #include <new>
 
 #include "tsg_common.cuh"
@@ -21,7 +22,17 @@ int fail(int code, const char *fmt, ...) {
 
 void clear_error() { g_err[0] = '\0'; }
 
+constexpr int64_t kPointLimit = (1LL << 32) - (1LL << 24);
+static std::atomic<int64_t> g_point_limit{kPointLimit};
+int64_t point_limit() { return g_point_limit.load(std::memory_order_relaxed); }
+
 }  // namespace tsg
+
+extern "C" int tsg_set_point_limit(int64_t n) {
+    if (n < 0 || n > tsg::kPointLimit) return tsg::fail(TSG_EVALUE, "point limit %lld out of range", (long long)n);
+    tsg::g_point_limit.store(n ? n : tsg::kPointLimit, std::memory_order_relaxed);
+    return TSG_OK;
+}
 
 extern "C" const char *tsg_last_error(void) { return tsg::g_err; }
 

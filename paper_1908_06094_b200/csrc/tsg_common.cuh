@@ -109,17 +109,34 @@ struct FastDiv {
     }
 };
 
-// (element, level) decomposition of a flat point index t = ((i*colors + c)*cols + j)*nk + k.
+// Points one launch may index with 32 bits (tsg_set_point_limit lowers it for tests).
+int64_t point_limit();
+
+// (element, level) decomposition of a flat point index t = ((i*colors + c)*cols + j)*nk + k
+// over a band of rows starting at row i0 (for_point_bands splits larger fields).
 struct PointDec {
     FastDiv nk, cols, colors;
-    uint32_t n;  // number of points (< 2^32)
+    uint32_t n;   // number of points of the band (< 2^32)
+    int i0;       // first row of the band
+    uint32_t e0;  // canonical id of its first element
     __host__ PointDec() {}
-    __host__ PointDec(int64_t rows, int ncols, int ncolors, int nlev)
-        : nk(nlev), cols(ncols), colors(ncolors), n((uint32_t)(rows * ncolors * ncols * nlev)) {}
+    __host__ PointDec(int64_t rows, int ncols, int ncolors, int nlev, int row0 = 0)
+        : nk(nlev), cols(ncols), colors(ncolors), n((uint32_t)(rows * ncolors * ncols * nlev)), i0(row0),
+          e0((uint32_t)((int64_t)row0 * ncolors * ncols)) {}
     static bool fits(int64_t rows, int ncols, int ncolors, int nlev) {
-        return rows * ncolors * ncols * nlev < (1LL << 32) - (1LL << 24);
+        return rows * ncolors * ncols * nlev < point_limit();
     }
 };
+
+// Launch fn(PointDec) over row bands that each fit a 32-bit point index: one band unless
+// the field has more than point_limit() points (an O1280 edge field at 137 levels has
+// 2.7e9; a 180 GB GPU holds patches of up to ~22 M vertices at that depth).
+template <class Fn>
+inline void for_point_bands(int64_t rows, int ncols, int ncolors, int nlev, Fn fn) {
+    const int64_t per_row = (int64_t)ncolors * ncols * nlev;
+    const int64_t band = std::max<int64_t>(1, point_limit() / std::max<int64_t>(1, per_row));
+    for (int64_t r = 0; r < rows; r += band) fn(PointDec(std::min(band, rows - r), ncols, ncolors, nlev, (int)r));
+}
 
 struct Pt {
     int i, c, j, k;
@@ -128,13 +145,14 @@ struct Pt {
 
 __device__ __forceinline__ Pt decompose(uint32_t t, const PointDec &D) {
     Pt p;
-    p.e = D.nk.div(t);
-    p.k = (int)(t - p.e * D.nk.d);
-    const uint32_t rest = D.cols.div(p.e);
-    p.j = (int)(p.e - rest * D.cols.d);
+    const uint32_t e = D.nk.div(t);
+    p.k = (int)(t - e * D.nk.d);
+    const uint32_t rest = D.cols.div(e);
+    p.j = (int)(e - rest * D.cols.d);
     const uint32_t i = D.colors.div(rest);
     p.c = (int)(rest - i * D.colors.d);
-    p.i = (int)i;
+    p.i = (int)i + D.i0;
+    p.e = e + D.e0;
     return p;
 }
 

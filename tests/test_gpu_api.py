@@ -741,3 +741,60 @@ def test_dealt_reduce_many_launches_stay_exact(cuda_ok):
         _lib.call("tsg_neighbor_reduce", g.handle, 0, 0, 33, _lib.ptr(src), None, _lib.ptr(dst), s)
         bad += (dst != ref).any()
     assert int(bad) == 0
+
+
+def test_point_bands_match_one_launch(cuda_ok):
+    """Fields with more points than one 32-bit-indexed launch covers are split into row
+    bands (tsg_common.cuh for_point_bands; ~10 M vertices x 137 levels for an edge field).
+    With the limit lowered to a few rows (tsg_set_point_limit), the reorders (pairs and
+    point forms), the synthetic fill and the unfused step give the one-launch result,
+    bitwise."""
+    import torch
+    from paper_1908_06094_b200 import _lib
+    from paper_1908_06094_b200.device import DeviceGrid
+
+    r, c, k = 23, 37, 20
+    g = DeviceGrid(r, c, k)
+    s = _lib.stream_handle()
+    rng = np.random.default_rng(0)
+    cases = [(L.EDGES.code, k), (L.CELLS.code, 7), (L.VERTICES.code, 1)]
+    flats = {(loc, inner): torch.from_numpy(rng.random((r * c * (3 if loc == 2 else 2 if loc == 1 else 1), inner)))
+             .cuda() for loc, inner in cases}
+    perm = {loc: torch.from_numpy(rng.permutation(len(f))).cuda() for (loc, _), f in flats.items()}
+
+    def run():
+        out = {}
+        for (loc, inner), flat in flats.items():
+            f = g.empty(loc, inner)
+            _lib.call("tsg_pack", g.handle, loc, inner, _lib.ptr(flat), _lib.ptr(perm[loc]), _lib.ptr(f), s)
+            back = torch.empty_like(flat)
+            _lib.call("tsg_unpack", g.handle, loc, inner, _lib.ptr(f), _lib.ptr(perm[loc]), _lib.ptr(back), s)
+            h = g.empty(loc, inner)
+            _lib.call("tsg_fill_hash", g.handle, loc, inner, 9, -1.0, 1.0, _lib.ptr(h), s)
+            out[loc, inner] = (f.clone(), back, h)
+        ins = {n: g.empty(loc, inner) for n, loc, inner in (("pd", 0, k), ("vn", 2, k), ("wn", 0, k + 1),
+                                                            ("rho", 0, k), ("signs", 0, 6), ("dual", 0, 1))}
+        inners = {"pd": k, "vn": k, "wn": k + 1, "rho": k, "signs": 6, "dual": 1}
+        for i, (n, t) in enumerate(ins.items()):
+            _lib.call("tsg_fill_hash", g.handle, 2 if n == "vn" else 0, inners[n], i,
+                      0.5 if n in ("rho", "dual") else -0.5, 1.5, _lib.ptr(t), s)
+        flux, fluz, div, pd_out = g.empty(2, k), g.empty(0, k + 1), g.empty(0, k), g.empty(0, k)
+        _lib.call("tsg_mpdata_step_unfused", g.handle, *[_lib.ptr(ins[n]) for n in ("pd", "vn", "wn", "rho",
+                                                                                    "signs", "dual")],
+                  _lib.ptr(flux), _lib.ptr(fluz), _lib.ptr(div), _lib.ptr(pd_out), 0.1, 0.7, 0, s)
+        out["step"] = (flux, fluz, div, pd_out)
+        torch.cuda.synchronize()
+        return out
+
+    want = run()
+    for k_i, f in flats.items():
+        assert torch.equal(want[k_i][1], f)  # pack -> unpack round trip
+    try:
+        for limit in (c * 7, c * 3 * 10 + 1, 1):  # a few rows per band, ragged bands, one row per band
+            _lib.call("tsg_set_point_limit", limit)
+            got = run()
+            for key in want:
+                for a, b in zip(want[key], got[key]):
+                    assert torch.equal(a, b), (limit, key)
+    finally:
+        _lib.call("tsg_set_point_limit", 0)

@@ -73,6 +73,9 @@ def test_argument_errors_map_to_reference_exceptions():
     # round-2 entry points validate before any device work
     with pytest.raises(ValueError, match="reduce variant"):
         _lib.check(lib.tsg_set_reduce_variant(20))
+    with pytest.raises(ValueError, match="point limit"):
+        _lib.check(lib.tsg_set_point_limit(-1))
+    _lib.check(lib.tsg_set_point_limit(0))
     with pytest.raises(ValueError, match="NULL"):
         _lib.check(lib.tsg_flat_flux(None, p, p, 4, 2, 0, p, None))
     with pytest.raises(ValueError, match="operator"):
