@@ -622,6 +622,104 @@ __global__ void __launch_bounds__(256) ifluz_pairs_kernel(uint32_t n, FastDiv np
 
 #undef TSG_FLAT_ITEMS
 
+// Point items (one thread per (row, level), kUnroll per thread per pass) for odd level
+// counts, whose flat rows are not 16-byte aligned (the cfg5 depth, K = 137): scalar loads,
+// a warp on 32 consecutive levels of a row (table entries broadcast).  Same operation
+// order as the level-pair forms.  n < 2^32 - 2^24 (point_limit()); 64-bit pass arithmetic.
+#define TSG_POINT_ITEMS(q, u, n)                                                                 \
+    const bool ch_ = (uint64_t)kUnroll * gridDim.x * blockDim.x >= (n);                         \
+    for (uint64_t base_ = (uint64_t)blockIdx.x * blockDim.x * (ch_ ? kUnroll : 1) + threadIdx.x, \
+                  T_ = ch_ ? blockDim.x : (uint64_t)gridDim.x * blockDim.x;                      \
+         base_ < (n); base_ += (uint64_t)kUnroll * gridDim.x * blockDim.x)                       \
+        _Pragma("unroll") for (int u = 0; u < kUnroll; ++u)                                       \
+            if (const uint64_t q64_ = base_ + u * T_; q64_ < (n))                                   \
+                if (const uint32_t q = (uint32_t)q64_; true)
+
+template <int OP>
+__global__ void __launch_bounds__(256) iflux_points_kernel(const int64_t *__restrict__ e2v, uint32_t n,
+                                                           FastDiv nk, const double *__restrict__ pd,
+                                                           const double *__restrict__ vn,
+                                                           double *__restrict__ flux) {
+    TSG_POINT_ITEMS(q, u, n) {
+        const uint32_t e = nk.div(q);
+        const int k = (int)(q - e * nk.d);
+        const int64_t o = __ldg(e2v + 2 * (int64_t)e), p = __ldg(e2v + 2 * (int64_t)e + 1);
+        flux[q] = edge_flux<OP>(pd[o * nk.d + k], pd[p * nk.d + k], vn[q]);
+    }
+}
+
+// The same over pairs of the flat [edge, level] array (16-byte vn loads and flux stores
+// whatever the row alignment; a pair may straddle two edges' rows); the pd gathers stay
+// scalar.
+template <int OP>
+__global__ void __launch_bounds__(256) iflux_flatpairs_kernel(const int64_t *__restrict__ e2v, uint32_t n,
+                                                              FastDiv nk, const double *__restrict__ pd,
+                                                              const double *__restrict__ vn,
+                                                              double *__restrict__ flux) {
+    const uint32_t n2 = (n + 1) / 2;
+    const int K = (int)nk.d;
+    TSG_POINT_ITEMS(m, u, n2) {
+        const uint32_t q0 = 2 * m;
+        const uint32_t e0 = nk.div(q0);
+        const int k0 = (int)(q0 - e0 * nk.d);
+        const int64_t o0 = __ldg(e2v + 2 * (int64_t)e0), p0 = __ldg(e2v + 2 * (int64_t)e0 + 1);
+        if (q0 + 1 < n) {
+            const bool next = k0 + 1 == K;  // the pair's second value opens the next edge's row
+            const int k1 = next ? 0 : k0 + 1;
+            const int64_t o1 = next ? __ldg(e2v + 2 * (int64_t)e0 + 2) : o0;
+            const int64_t p1 = next ? __ldg(e2v + 2 * (int64_t)e0 + 3) : p0;
+            const double2 v = ld2(vn + q0);
+            st2(flux + q0, make_double2(edge_flux<OP>(pd[o0 * K + k0], pd[p0 * K + k0], v.x),
+                                        edge_flux<OP>(pd[o1 * K + k1], pd[p1 * K + k1], v.y)));
+        } else {
+            flux[q0] = edge_flux<OP>(pd[o0 * K + k0], pd[p0 * K + k0], vn[q0]);
+        }
+    }
+}
+
+// ADV = false: the divergence alone (reference.py:63-79)
+template <bool ADV>
+__global__ void __launch_bounds__(256) idiv_advance_points_kernel(
+    const int64_t *__restrict__ v2e, uint32_t n, FastDiv nk, double dt, const double *__restrict__ signs,
+    const double *__restrict__ dual, const double *__restrict__ flux, const double *__restrict__ fluz,
+    const double *__restrict__ pd, const double *__restrict__ rho, double *__restrict__ div,
+    double *__restrict__ pd_out) {
+    const int K = (int)nk.d;
+    TSG_POINT_ITEMS(q, u, n) {
+        const uint32_t v = nk.div(q);
+        const int k = (int)(q - v * nk.d);
+        double acc = 0.0;
+#pragma unroll
+        for (int s = 0; s < 6; ++s)
+            acc = add(mul(__ldg(signs + (int64_t)v * 6 + s), flux[__ldg(v2e + (int64_t)v * 6 + s) * K + k]), acc);
+        const double *Z = fluz + (int64_t)v * (K + 1) + k;
+        acc = add(acc, sub(Z[1], Z[0]));
+        const double d = dvd(acc, __ldg(dual + v));
+        div[q] = d;
+        if constexpr (ADV) pd_out[q] = sub(pd[q], dvd(mul(dt, d), rho[q]));
+    }
+}
+
+__global__ void __launch_bounds__(256) icell_div_points_kernel(const int64_t *__restrict__ c2e, uint32_t n,
+                                                               FastDiv nk, const double *__restrict__ vn,
+                                                               const double *__restrict__ length,
+                                                               const double *__restrict__ area,
+                                                               double *__restrict__ out) {
+    const int K = (int)nk.d;
+    TSG_POINT_ITEMS(q, u, n) {
+        const uint32_t c = nk.div(q);
+        const int k = (int)(q - c * nk.d);
+        double acc = 0.0;
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+            const int64_t e = __ldg(c2e + (int64_t)c * 3 + s);
+            acc = add(mul(vn[e * K + k], __ldg(length + e)), acc);
+        }
+        out[q] = dvd(acc, __ldg(area + c));
+    }
+}
+#undef TSG_POINT_ITEMS
+
 }  // namespace tsg
 
 using namespace tsg;
@@ -794,6 +892,23 @@ extern "C" int tsg_mpdata_step_unfused(const tsg_grid *g, const double *pd, cons
     return TSG_OK;
 }
 
+// odd level counts / unaligned rows: flat pairs when vn and flux are 16-byte aligned
+static void launch_iflux_points(int flux_op, const int64_t *e2v, uint32_t nE, int nlev, const double *pd,
+                                const double *vn, double *flux, int sms, cudaStream_t st) {
+    const bool pairs = (reinterpret_cast<uintptr_t>(vn) % 16) == 0 && (reinterpret_cast<uintptr_t>(flux) % 16) == 0;
+    auto go = [&](auto kernel, uint32_t items) {
+        kernel<<<item_grid((const void *)kernel, items, kUnroll, sms), 256, 0, st>>>(e2v, nE, FastDiv(nlev), pd, vn,
+                                                                                     flux);
+    };
+    if (pairs) {
+        if (flux_op == TSG_UPWIND) go(iflux_flatpairs_kernel<TSG_UPWIND>, (nE + 1) / 2);
+        else go(iflux_flatpairs_kernel<TSG_CENTRED>, (nE + 1) / 2);
+    } else {
+        if (flux_op == TSG_UPWIND) go(iflux_points_kernel<TSG_UPWIND>, nE);
+        else go(iflux_points_kernel<TSG_CENTRED>, nE);
+    }
+}
+
 extern "C" int tsg_transport_indirect(const int64_t *e2v, const int64_t *v2e, const double *signs,
                                       const double *dual, const double *pd, const double *vn,
                                       const double *wn, const double *rho, int64_t nv, int64_t ne,
@@ -828,6 +943,19 @@ extern "C" int tsg_transport_indirect(const int64_t *e2v, const int64_t *v2e, co
         TSG_CHECK_LAUNCH();
         return TSG_OK;
     }
+    if (ne * (int64_t)nlev < point_limit() && nv * (int64_t)(nlev / 2 + 1) < (1LL << 31)) {
+        // odd level counts (rows not 16-byte aligned): point items, any alignment
+        const uint32_t nE = (uint32_t)(ne * nlev), nV = (uint32_t)(nv * nlev);
+        const uint32_t nZ = (uint32_t)(nv * (nlev / 2 + 1));
+        launch_iflux_points(flux_op, e2v, nE, nlev, pd, vn, flux, sms, st);
+        ifluz_pairs_kernel<<<item_grid((const void *)ifluz_pairs_kernel, nZ, kUnroll, sms), 256, 0, st>>>(
+            nZ, FastDiv(nlev / 2 + 1), nlev, pivbz, pd, wn, fluz);
+        idiv_advance_points_kernel<true><<<item_grid((const void *)idiv_advance_points_kernel<true>, nV, kUnroll, sms),
+                                           256, 0, st>>>(v2e, nV, FastDiv(nlev), dt, signs, dual, flux, fluz, pd, rho,
+                                                         div, pd_out);
+        TSG_CHECK_LAUNCH();
+        return TSG_OK;
+    }
     if (flux_op == TSG_UPWIND)
         launch_rows(iflux_kernel<TSG_UPWIND>, ne, sms, st, e2v, ne, nlev, pd, vn, flux);
     else
@@ -859,6 +987,9 @@ extern "C" int tsg_flat_flux(const int64_t *e2v, const double *pd, const double 
         else
             iflux_pairs_kernel<TSG_CENTRED><<<item_grid((const void *)iflux_pairs_kernel<TSG_CENTRED>, nE, kUnroll,
                                                             sms), 256, 0, st>>>(e2v, nE, FastDiv(np), nlev, pd, vn, flux);
+    } else if (ne * (int64_t)nlev < point_limit()) {
+        const uint32_t nE = (uint32_t)(ne * nlev);
+        launch_iflux_points(flux_op, e2v, nE, nlev, pd, vn, flux, sms, st);
     } else if (flux_op == TSG_UPWIND) {
         launch_rows(iflux_kernel<TSG_UPWIND>, ne, sms, st, e2v, ne, nlev, pd, vn, flux);
     } else {
@@ -899,6 +1030,11 @@ extern "C" int tsg_flat_divergence(const int64_t *v2e, int width, const double *
         idiv_advance_pipe_kernel<false><<<item_grid((const void *)idiv_advance_pipe_kernel<false>, n, 1, sm_count(),
                                                     true), 256, 0, (cudaStream_t)s>>>(
             v2e, n, FastDiv(nlev / 2), nlev, 0.0, signs, dual, flux, fluz, nullptr, nullptr, div, nullptr);
+    } else if (width == 6 && nv * (int64_t)nlev < point_limit()) {
+        const uint32_t n = (uint32_t)(nv * nlev);
+        idiv_advance_points_kernel<false><<<item_grid((const void *)idiv_advance_points_kernel<false>, n, kUnroll,
+                                                      sm_count()), 256, 0, (cudaStream_t)s>>>(
+            v2e, n, FastDiv(nlev), 0.0, signs, dual, flux, fluz, nullptr, nullptr, div, nullptr);
     } else {
         launch_rows(idiv_kernel, nv, sm_count(), (cudaStream_t)s, v2e, width, nv, nlev, signs, dual, flux, fluz,
                     div);
@@ -935,6 +1071,10 @@ extern "C" int tsg_flat_cell_divergence(const int64_t *c2e, int width, const dou
         const uint32_t n = (uint32_t)(nc * (nlev / 2));
         icell_div_pipe_kernel<<<item_grid((const void *)icell_div_pipe_kernel, n, 1, sm_count(), true), 256, 0,
                                 (cudaStream_t)s>>>(c2e, n, FastDiv(nlev / 2), nlev, vn, length, area, out);
+    } else if (width == 3 && nc * (int64_t)nlev < point_limit()) {
+        const uint32_t n = (uint32_t)(nc * nlev);
+        icell_div_points_kernel<<<item_grid((const void *)icell_div_points_kernel, n, kUnroll, sm_count()), 256, 0,
+                                  (cudaStream_t)s>>>(c2e, n, FastDiv(nlev), vn, length, area, out);
     } else {
         launch_rows(icell_div_kernel, nc, sm_count(), (cudaStream_t)s, c2e, width, nc, nlev, vn, length, area,
                     out);

@@ -65,12 +65,14 @@ def test_flat_stages_match_oracle(cuda_ok, shape, relabel):
     assert np.array_equal(R.neighbor_sum_scaled(c2c, a, fac), O.neighbor_sum_scaled(c2c, a, fac))
 
 
-def test_flat_stages_long_sweeps(cuda_ok):
-    """A patch whose level-pair sweeps are long enough for one-pass grids (tsg_common.cuh
-    item_grid) and the pipelined divergence / cell-divergence gathers: each stage, bitwise."""
+@pytest.mark.parametrize("k", [40, 41])
+def test_flat_stages_long_sweeps(cuda_ok, k):
+    """A patch whose item sweeps are long enough for one-pass grids (tsg_common.cuh
+    item_grid): the level-pair forms and pipelined gathers (even level count) and the point
+    forms (odd: rows not 16-byte aligned), each stage and the whole step, bitwise."""
     import torch
 
-    r, c, k = 1024, 1024, 40
+    r, c = 1024, 1024
     inp = O.transport_inputs(r, c, k, 2, "random", "random", "random")
     e2v = O.neighbor_table(r, c, "edges", "vertices")
     v2e = O.neighbor_table(r, c, "vertices", "edges")
@@ -93,6 +95,13 @@ def test_flat_stages_long_sweeps(cuda_ok):
     area = 0.2 + np.random.default_rng(4).random(len(c2e))
     got = R.cell_divergence(dev["c2e"], dev["vn"], torch.from_numpy(length).cuda(), torch.from_numpy(area).cuda())
     assert np.array_equal(got.cpu().numpy(), O.cell_divergence(c2e, inp["vn"], length, area))
+    got = R.upwind_flux(dev["e2v"], dev["vn"], dev["pd"])
+    assert np.array_equal(got.cpu().numpy(), flux)
+    step = R.transport_step(dev["e2v"], dev["v2e"], dev["signs"], dev["dual"], dev["pd"], dev["vn"], dev["wn"],
+                            dev["rho"], 0.1, 0.5)
+    got = step["pd_out"]
+    got = got.cpu().numpy() if hasattr(got, "cpu") else got
+    assert np.array_equal(got, O.advance_density(inp["pd"], div, inp["rho"], 0.1))
 
 
 def test_one_dimensional_arrays_and_device_tensors(cuda_ok):

@@ -1,2 +1,3 @@
-nvidia-smi --query-gpu=name,memory.total --format=csv,noheader
-for sz in "4096 4096 137 10" "3300 3300 137 10" "2560 2576 137 10"; do timeout 900 python tools/big_patch_probe.py $sz 2>&1 | tail -1; done
+timeout 900 python -m pytest tests/test_gpu_reference_api.py tests/test_gpu_parity.py -x -q 2>&1 | tail -2
+timeout 900 python tools/flat_stages_probe.py 1024 1024 81 2>&1 | grep flux
+for sz in "2560 2576 137" "1024 1024 81" "279 256 79"; do timeout 900 python tools/indirect_step_probe.py $sz 2>&1 | tail -1; done
