@@ -648,6 +648,67 @@ __global__ void __launch_bounds__(256) iflux_points_kernel(const int64_t *__rest
     }
 }
 
+// Table-1 gather (reference.neighbor_sum(_scaled), reference.py:137-157) at odd level
+// counts: pairs of the flat [row, level] output (16-byte stores; a pair may straddle two
+// rows, whose table entries are then both read), scalar neighbour gathers, the next
+// pair's table entries fetched while this pair's gathers are in flight (the even-level
+// pipeline's scheme; one pair per thread per iteration on a resident grid).
+template <int W, bool SCALE>
+__global__ void __launch_bounds__(256) reduce_indirect_flatpairs_kernel(const int64_t *__restrict__ table,
+                                                                        uint32_t n, FastDiv nk,
+                                                                        const double *__restrict__ src,
+                                                                        const double *__restrict__ scale,
+                                                                        double *__restrict__ dst) {
+    const uint32_t n2 = (n + 1) / 2, T = gridDim.x * blockDim.x;
+    const int K = (int)nk.d;
+    int64_t nb0[W], nb1[W];
+    uint32_t r0 = 0;
+    int k0 = 0;
+    bool next = false;
+    double sc0 = 1.0, sc1 = 1.0;
+    auto fetch = [&](uint32_t m) {
+        const uint32_t q0 = 2 * m;
+        r0 = nk.div(q0);
+        k0 = (int)(q0 - r0 * nk.d);
+        next = k0 + 1 == K && q0 + 1 < n;
+#pragma unroll
+        for (int s = 0; s < W; ++s) nb0[s] = __ldg(table + (int64_t)r0 * W + s);
+#pragma unroll
+        for (int s = 0; s < W; ++s) nb1[s] = next ? __ldg(table + (int64_t)(r0 + 1) * W + s) : nb0[s];
+        if (SCALE) {
+            sc0 = __ldg(scale + r0);
+            sc1 = next ? __ldg(scale + r0 + 1) : sc0;
+        }
+    };
+    uint32_t m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m < n2) fetch(m);
+    for (; m < n2; m += T) {
+        const uint32_t q0 = 2 * m;
+        const bool two = q0 + 1 < n, nx = next;
+        const double s0 = sc0, s1 = sc1;
+        const int kc = k0, k1 = nx ? 0 : k0 + 1;
+        double v0[W], v1[W];
+#pragma unroll
+        for (int s = 0; s < W; ++s) {
+            v0[s] = src[nb0[s] * K + kc];
+            v1[s] = two ? src[nb1[s] * K + k1] : 0.0;
+        }
+        if (m + T < n2) fetch(m + T);
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int s = 0; s < W; ++s) {
+            a0 = add(v0[s], a0);
+            a1 = add(v1[s], a1);
+        }
+        if (SCALE) {
+            a0 = mul(a0, s0);
+            a1 = mul(a1, s1);
+        }
+        if (two) st2(dst + q0, make_double2(a0, a1));
+        else dst[q0] = a0;
+    }
+}
+
 // The same over pairs of the flat [edge, level] array (16-byte vn loads and flux stores
 // whatever the row alignment; a pair may straddle two edges' rows); the pd gathers stay
 // scalar.
@@ -803,6 +864,31 @@ extern "C" int tsg_neighbor_reduce_indirect(const int64_t *table, int64_t nrows,
                 case 3: go(reduce_indirect_pipe_kernel<3, false, 1>); break;
                 case 4: go(reduce_indirect_pipe_kernel<4, false, 1>); break;
                 default: go(reduce_indirect_pipe_kernel<6, false, 1>); break;
+            }
+        }
+        TSG_CHECK_LAUNCH();
+        return TSG_OK;
+    }
+    if ((reinterpret_cast<uintptr_t>(dst) % 16) == 0 && nrows * (int64_t)nlev < point_limit() &&
+        (width == 2 || width == 3 || width == 4 || width == 6)) {  // odd level counts
+        const uint32_t n = (uint32_t)(nrows * nlev);
+        auto go = [&](auto kernel) {
+            kernel<<<item_grid((const void *)kernel, (n + 1) / 2, 1, sms, true), 256, 0, st>>>(
+                table, n, FastDiv((uint32_t)nlev), src, scale, dst);
+        };
+        if (scale) {
+            switch (width) {
+                case 2: go(reduce_indirect_flatpairs_kernel<2, true>); break;
+                case 3: go(reduce_indirect_flatpairs_kernel<3, true>); break;
+                case 4: go(reduce_indirect_flatpairs_kernel<4, true>); break;
+                default: go(reduce_indirect_flatpairs_kernel<6, true>); break;
+            }
+        } else {
+            switch (width) {
+                case 2: go(reduce_indirect_flatpairs_kernel<2, false>); break;
+                case 3: go(reduce_indirect_flatpairs_kernel<3, false>); break;
+                case 4: go(reduce_indirect_flatpairs_kernel<4, false>); break;
+                default: go(reduce_indirect_flatpairs_kernel<6, false>); break;
             }
         }
         TSG_CHECK_LAUNCH();

@@ -1,5 +1,6 @@
 """The reference's flat stages one at a time (reference.py:18-90, 119-134) through the C ABI
-(tsg_flat_flux / _fluz / _divergence / _advance / _cell_divergence) on flat canonical arrays:
+(tsg_flat_flux / _fluz / _divergence / _advance / _cell_divergence, and the Table-1 gathers
+tsg_neighbor_reduce_indirect) on flat canonical arrays:
 time per call after an L2 flush (mean of 50) and the fraction of the measured copy peak
 for each stage's DISTINCT bytes.   python tools/flat_stages_probe.py [rows cols K]"""
 import json
@@ -39,6 +40,7 @@ nv, ne, nc = R * C, 3 * R * C, 2 * R * C
 e2v = build_neighbor_table(spec, L.EDGES, L.VERTICES, as_tensor=True).ids
 v2e = build_neighbor_table(spec, L.VERTICES, L.EDGES, as_tensor=True).ids
 c2e = build_neighbor_table(spec, L.CELLS, L.EDGES, as_tensor=True).ids
+c2c = build_neighbor_table(spec, L.CELLS, L.CELLS, as_tensor=True).ids
 f64 = dict(dtype=torch.float64, device="cuda")
 pd, rho = torch.rand(nv, K, **f64) + 0.5, torch.rand(nv, K, **f64) + 0.5
 vn, wn = torch.rand(ne, K, **f64) - 0.5, torch.rand(nv, K + 1, **f64) - 0.5
@@ -47,6 +49,7 @@ length, area = torch.rand(ne, **f64) + 0.5, torch.rand(nc, **f64) + 0.5
 flux, fluz, div, out = torch.empty(ne, K, **f64), torch.empty(nv, K + 1, **f64), torch.empty(nv, K, **f64), \
     torch.empty(nv, K, **f64)
 cdiv = torch.empty(nc, K, **f64)
+ca, cb, fac = torch.rand(nc, K, **f64), torch.empty(nc, K, **f64), torch.rand(nc, **f64) + 0.5
 s = _lib.stream_handle()
 p = _lib.ptr
 stages = {
@@ -62,6 +65,10 @@ stages = {
     "flat_cell_divergence": (lambda: _lib.call("tsg_flat_cell_divergence", p(c2e), 3, p(vn), p(length), p(area), nc, K,
                                                p(cdiv), s),
                              8 * (nc * 3 + ne * K + ne + nc + nc * K)),
+    "flat_neighbor_sum": (lambda: _lib.call("tsg_neighbor_reduce_indirect", p(c2c), nc, 3, K, p(ca), None, p(cb), s),
+                          8 * 2 * nc * K),
+    "flat_neighbor_sum_scaled": (lambda: _lib.call("tsg_neighbor_reduce_indirect", p(c2c), nc, 3, K, p(ca), p(fac),
+                                                   p(cb), s), 8 * (2 * nc * K + nc)),
 }
 for name, (fn, nbytes) in stages.items():
     t = timed(fn)
