@@ -1,2 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_reference_api.py tests/test_gpu_api.py tests/test_gpu_parity.py -x -q -k "neighbor or table1 or flat or one_dim or relabel or reduce" 2>&1 | tail -2
-for sz in "1024 1024 81" "1024 1024 80" "128 128 81"; do timeout 900 python tools/flat_stages_probe.py $sz 2>&1 | grep neighbor; done
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 1500 compute-sanitizer --tool memcheck --print-limit 10 python -m pytest tests/test_gpu_reference_api.py tests/test_gpu_acceptance.py -x -q -k "not long_sweeps" > gpurun_out/san_flat_memcheck.log 2>&1; echo "memcheck rc=$?"; tail -3 gpurun_out/san_flat_memcheck.log
+timeout 900 compute-sanitizer --tool memcheck python tools/indirect_step_probe.py 37 45 21 2>&1 | tail -2
