@@ -89,7 +89,10 @@ constexpr int kItemUnroll = 4;
 // against 445-470 us with two items, 520-540 with three and 529-548 us for round 1's
 // unpipelined four (tools/pack_variants.py, TSG_PACK_V A/B build).
 constexpr int kPackUnroll = 1;
-template <int U>
+// FA = false: an odd level count (flat rows not 16-byte aligned) -- the flat side is read
+// as two scalars, the field side still stored as aligned pairs (even pitch), the last
+// pair's second value (the first padding slot) as 0.
+template <int U, bool FA = true>
 __global__ void __launch_bounds__(256) pack_pairs_kernel(FieldIx F, int inner, PointDec D,
                                                          const double *__restrict__ flat,
                                                          const int64_t *__restrict__ forward,
@@ -116,7 +119,12 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(FieldIx F, int inner, P
 #pragma unroll
         for (int u = 0; u < kItemUnroll; ++u) {
             if (base + u * T < D.n) {
-                v[u] = __ldg(reinterpret_cast<const double2 *>(flat + rank[u] * inner + 2 * p[u].k));
+                if constexpr (FA) {
+                    v[u] = __ldg(reinterpret_cast<const double2 *>(flat + rank[u] * inner + 2 * p[u].k));
+                } else {
+                    const double *row = flat + rank[u] * inner + 2 * p[u].k;
+                    v[u] = make_double2(__ldg(row), 2 * p[u].k + 1 < inner ? __ldg(row + 1) : 0.0);
+                }
                 q[u] = p[u];
             }
         }
@@ -129,6 +137,7 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(FieldIx F, int inner, P
     }
 }
 
+template <bool FA = true>
 __global__ void __launch_bounds__(256) unpack_pairs_kernel(FieldIx F, int inner, PointDec D,
                                                            const double *__restrict__ f,
                                                            const int64_t *__restrict__ forward,
@@ -149,11 +158,30 @@ __global__ void __launch_bounds__(256) unpack_pairs_kernel(FieldIx F, int inner,
         for (int u = 0; u < kItemUnroll; ++u) {
             if (base + u * T >= D.n) break;
             const int64_t rank = forward ? __ldg(forward + p[u].e) : p[u].e;
-            st2(flat + rank * inner + 2 * p[u].k, v[u]);
+            if constexpr (FA) {
+                st2(flat + rank * inner + 2 * p[u].k, v[u]);
+            } else {
+                double *row = flat + rank * inner + 2 * p[u].k;
+                row[0] = v[u].x;
+                if (2 * p[u].k + 1 < inner) row[1] = v[u].y;
+            }
         }
     }
 }
 
+// Grids of the level-pair reorders.  Long sweeps (more than 16 passes of one resident wave,
+// item_grid's rule) take one pass per block -- O1280 edge field at 137 levels: pack 8.0 vs
+// 10.2 ms, unpack 6.5 vs 9.3 ms; at 136 levels unpack 6.4 vs 7.5 ms -- against grid_for's
+// 16 blocks per SM walking the field in grid-stride passes, which stays ahead on short
+// sweeps (279x256x80 unpack 42.6 vs 44.8 us) and for the even pack, whose pipelined rank
+// fetch wants several items per thread (tools/reorder_probe.py).
+static unsigned reorder_grid(const void *kernel, int64_t n, int per, int num_sms) {
+    const unsigned g = item_grid(kernel, n, per, num_sms);
+    return (int64_t)g * 256 * per >= n ? g : (unsigned)grid_for((n + per - 1) / per, 256, num_sms);
+}
+#define TSG_ODD_GRID(K, n, per) reorder_grid((const void *)K, n, per, g->num_sms)
+#define TSG_EVEN_GRID(K, n, per, persist) \
+    ((persist) ? (unsigned)grid_for(((n) + (per) - 1) / (per), 256, g->num_sms) : reorder_grid((const void *)K, n, per, g->num_sms))
 static bool pairs_ok(int inner, const void *flat) {
     return inner >= 16 && (inner & 1) == 0 && (reinterpret_cast<uintptr_t>(flat) % 16) == 0;
 }
@@ -491,9 +519,15 @@ extern "C" int tsg_pack(const tsg_grid *g, int loc, int inner, const double *fla
     FieldIx F(g->rows, g->cols, colors_of(loc), inner);
     if (pairs_ok(inner, flat)) {
         for_point_bands(g->rows, g->cols, F.colors, inner / 2, [&](const PointDec &Dp) {
-            pack_pairs_kernel<kPackUnroll><<<grid_for((Dp.n + kPackUnroll - 1) / kPackUnroll, 256, g->num_sms),
+            pack_pairs_kernel<kPackUnroll><<<TSG_EVEN_GRID((pack_pairs_kernel<kPackUnroll>), Dp.n, kPackUnroll, true),
                                              256, 0, (cudaStream_t)s>>>(F, inner, Dp, flat, forward, field,
                                                                         g->flags);
+        });
+    } else if (inner >= 16 && (inner & 1)) {  // odd: scalar flat side, aligned field pairs
+        for_point_bands(g->rows, g->cols, F.colors, (inner + 1) / 2, [&](const PointDec &Dp) {
+            pack_pairs_kernel<kPackUnroll, false><<<TSG_ODD_GRID((pack_pairs_kernel<kPackUnroll, false>), Dp.n, 1), 256, 0,
+                                                   (cudaStream_t)s>>>(
+                F, inner, Dp, flat, forward, field, g->flags);
         });
     } else if (inner >= 16) {
         launch_lines(pack_lines_kernel, g->cols, (int64_t)g->rows * F.colors, g->num_sms,
@@ -516,8 +550,13 @@ extern "C" int tsg_unpack(const tsg_grid *g, int loc, int inner, const double *f
     FieldIx F(g->rows, g->cols, colors_of(loc), inner);
     if (pairs_ok(inner, flat)) {
         for_point_bands(g->rows, g->cols, F.colors, inner / 2, [&](const PointDec &Dp) {
-            unpack_pairs_kernel<<<grid_for((Dp.n + kItemUnroll - 1) / kItemUnroll, 256, g->num_sms), 256, 0,
+            unpack_pairs_kernel<<<TSG_EVEN_GRID((unpack_pairs_kernel<true>), Dp.n, kItemUnroll, false), 256, 0,
                                   (cudaStream_t)s>>>(F, inner, Dp, field, forward, flat);
+        });
+    } else if (inner >= 16 && (inner & 1)) {  // odd: aligned field pairs, scalar flat side
+        for_point_bands(g->rows, g->cols, F.colors, (inner + 1) / 2, [&](const PointDec &Dp) {
+            unpack_pairs_kernel<false><<<TSG_ODD_GRID((unpack_pairs_kernel<false>), Dp.n, kItemUnroll), 256, 0,
+                                         (cudaStream_t)s>>>(F, inner, Dp, field, forward, flat);
         });
     } else if (inner >= 16) {
         launch_lines(unpack_lines_kernel, g->cols, (int64_t)g->rows * F.colors, g->num_sms,

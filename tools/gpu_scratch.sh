@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout 1500 compute-sanitizer --tool memcheck --print-limit 10 python -m pytest tests/test_gpu_reference_api.py tests/test_gpu_acceptance.py -x -q -k "not long_sweeps" > gpurun_out/san_flat_memcheck.log 2>&1; echo "memcheck rc=$?"; tail -3 gpurun_out/san_flat_memcheck.log
-timeout 900 compute-sanitizer --tool memcheck python tools/indirect_step_probe.py 37 45 21 2>&1 | tail -2
+timeout 900 python -m pytest tests -m gpu -x -q -k "pack or reorder or layout or strided or stream or relabel or point_bands or acceptance" 2>&1 | tail -2
+for sz in "2560 2576 137" "2560 2576 136" "1024 1024 81" "1024 1024 80" "279 256 80" "279 256 79"; do timeout 900 python tools/reorder_probe.py $sz 2 2>&1 | grep '"sn"'; done
