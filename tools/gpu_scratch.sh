@@ -1,2 +1,5 @@
-timeout 900 python -m pytest tests/test_gpu_reference_api.py -x -q 2>&1 | tail -2
-for sz in "1024 1024 81" "279 256 79"; do timeout 900 python tools/flat_stages_probe.py $sz 2>&1 | grep cell_div; done
+bash tools/gpu_round.sh > gpurun_out/round2.log 2>&1
+cp gpurun_out/bench.log gpurun_out/bench_r2f.log; cp gpurun_out/bench_ref.log gpurun_out/bench_ref_r2f.log
+grep -E "passed|failed|error" gpurun_out/gputest.log | tail -2; tail -1 gpurun_out/smoke.log
+python tools/bench_brief.py gpurun_out/bench.log
+tail -c 400 gpurun_out/bench_ref.log; echo; tail -c 300 gpurun_out/bench2.log
